@@ -1,0 +1,104 @@
+// Device helpers shared by the simulation, SVD and overlap kernels:
+// complex128 arithmetic on double2, CTA/warp-group reductions.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mpskq {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ double2 cz() { return make_double2(0.0, 0.0); }
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+__device__ __forceinline__ double2 csub(double2 a, double2 b) {
+  return make_double2(a.x - b.x, a.y - b.y);
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) {
+  return make_double2(a.x * s, a.y * s);
+}
+// a * b
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// acc + a * b  (4 DFMA)
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 acc) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+  return acc;
+}
+// acc + conj(a) * b  (4 DFMA)
+__device__ __forceinline__ double2 cfmac(double2 a, double2 b, double2 acc) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+  return acc;
+}
+__device__ __forceinline__ double cnorm2(double2 a) { return fma(a.x, a.x, a.y * a.y); }
+__device__ __forceinline__ bool cfinite(double2 a) { return isfinite(a.x) && isfinite(a.y); }
+
+template <int NT>
+__device__ __forceinline__ void bsync() {
+  if constexpr (NT == 32)
+    __syncwarp();
+  else
+    __syncthreads();
+}
+
+template <int NT>
+__device__ __forceinline__ int block_any(int v) {
+  if constexpr (NT == 32) {
+    __syncwarp();
+    return __any_sync(kFull, v);
+  } else
+    return __syncthreads_or(v);
+}
+
+// sum over aligned groups of G lanes (G a power of two <= 32); every lane of
+// the warp must call it.  The xor butterfly gives all lanes of a group the
+// bitwise-identical result.
+__device__ __forceinline__ double group_sum(double v, int G) {
+  for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+__device__ __forceinline__ double2 group_sum(double2 v, int G) {
+  for (int o = G >> 1; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(kFull, v.x, o);
+    v.y += __shfl_xor_sync(kFull, v.y, o);
+  }
+  return v;
+}
+
+// CTA-wide sum, identical on every thread.  `red` needs NT/32 doubles.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  v = group_sum(v, 32);
+  if constexpr (NT == 32) {
+    return v;
+  } else {
+    const int w = threadIdx.x >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[w] = v;
+    __syncthreads();
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) s += red[i];
+    return s;
+  }
+}
+
+// lanes per work item so that G * items <= NT, G in [1, 32]
+template <int NT>
+__device__ __forceinline__ int group_width(int items) {
+  int G = 32;
+  while (G > 1 && G * items > NT) G >>= 1;
+  return G;
+}
+
+}  // namespace mpskq

@@ -1,0 +1,84 @@
+// Internal declarations shared by the host runtime (runtime.cpp) and the CUDA
+// translation units.  Nothing here crosses the C ABI.
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include "mpskq.h"
+
+namespace mpskq {
+
+// thread-local last error; returns `status` so callers can `return fail(...)`
+int fail(int status, const char* fmt, ...);
+int cuda_fail(int err, const char* what);  // err is a cudaError_t
+
+// chi capacities with a compiled simulation + overlap path
+constexpr int kChiCaps[] = {4, 8, 16, 32};
+constexpr int kNumChiCaps = 4;
+inline bool chi_cap_supported(int c) {
+  for (int x : kChiCaps)
+    if (x == c) return true;
+  return false;
+}
+
+// layout helper (also used on device through the site_off table)
+int64_t bond_cap(int m, int chi_cap, int b);
+
+struct SimArgs {
+  int m;
+  int chi_cap;
+  const int32_t* ops;  // n_ops x 4
+  int64_t n_ops;
+  int64_t n_gates;
+  const double* coef;  // n_states x n_params x 2
+  int64_t n_params;
+  int64_t n_states;
+  double budget;
+  int chi_max;
+  const int64_t* site_off;
+  int64_t state_stride;
+  double* sites;
+  int32_t* chi;
+  double* discard;
+  int32_t* peak;
+  int32_t* status;
+  int64_t* entry_log;
+};
+int launch_simulate(const SimArgs& a, void* stream);
+
+struct SvdArgs {
+  int rows, cols;
+  int64_t batch;
+  const double* mats;
+  double budget;
+  int chi_max;
+  double *u, *s, *vh;
+  int32_t* keep;
+  double* discarded;
+  int32_t* status;
+};
+int launch_svd(const SvdArgs& a, void* stream);
+
+struct OverlapArgs {
+  int kind, out_mode, m, chi_cap;
+  const int64_t* site_off;
+  int64_t state_stride;
+  const double* bra_sites;
+  const int32_t* bra_chi;
+  int64_t n_bras;
+  const double* ket_sites;
+  const int32_t* ket_chi;
+  int64_t n_kets;
+  int rank, world;
+  double* out;
+  int64_t ld;
+};
+int launch_overlap(const OverlapArgs& a, void* stream);
+
+int launch_encode(const double* X, int64_t n_rows, int m, int r, int d, double gamma, double* coef,
+                  int* bad, void* stream);
+
+int launch_fp64_probe(int n_blocks, int64_t iters, double* out, void* stream);
+
+}  // namespace mpskq

@@ -1,0 +1,462 @@
+// Tiled batched MPS overlaps <bra_i|ket_j> and kernel entries |.|^2.
+//
+// Reference: inner_product (mps.py:260-268) — env = [[1]]; per site
+//   tmp = tensordot(env, conj(A), (0,0)); env = tensordot(tmp, B, ((0,1),(0,1)))
+// and compute_gram (kernel.py:147-185): train fills i<j, mirrors, diagonal 1.
+//
+// Two B200 paths:
+//  * small chi (capacity 4, the 165-qubit headline): one thread per (bra, ket)
+//    pair with its 4x4 complex environment in registers; a warp is one bra x 32
+//    kets, a CTA 8 bras x 32 kets.  Sites are repacked once into a
+//    lane-interleaved, zero-padded layout [site][ket block][entry][lane] so the
+//    32 kets of a warp read one coalesced 512-byte line per tensor entry, and
+//    the bra tensor of each site is staged once per warp in shared memory and
+//    read as broadcasts.  Loop bounds are the bra's exact bond dims and the
+//    ket block's maximum bond dims, both warp-uniform, so there is no
+//    divergence and padding costs only up to the block maximum.  Pure FP64
+//    FMA issue; no tensor cores (tcgen05 has no FP64 kind; DMMA only pays
+//    off for dense chi >= 16 contractions).
+//  * generic chi (capacities 8..32): one warp per pair, environments and
+//    intermediates in shared memory, exact bond dims from the batch layout.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "device.cuh"
+#include "internal.h"
+
+namespace mpskq {
+
+namespace {
+
+constexpr int kLanes = 32;
+constexpr int kP = 4;                  // padded chi of the small-chi path
+constexpr int kEnt = kP * 2 * kP;      // entries per padded site tensor (32)
+constexpr int kWarpsO1 = 8;            // bras per CTA tile
+
+// --------------------------------------------------------------- packing
+// sim layout -> [site][block][entry][lane] (double2), zero padded to 4x2x4
+__global__ void pack_o1_kernel(const double2* __restrict__ sites, const int32_t* __restrict__ chi,
+                               const int64_t* __restrict__ site_off, int64_t stride, int m,
+                               int64_t n, int64_t nblk, double2* __restrict__ out) {
+  const int64_t total = (int64_t)m * nblk * kEnt * kLanes;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = (int)(idx % kLanes);
+    const int e = (int)((idx / kLanes) % kEnt);
+    const int64_t blk = (idx / (kLanes * kEnt)) % nblk;
+    const int s = (int)(idx / ((int64_t)kLanes * kEnt * nblk));
+    const int64_t state = blk * kLanes + lane;
+    double2 v = make_double2(0.0, 0.0);
+    if (state < n) {
+      const int k = e / (2 * kP), p = (e / kP) & 1, r = e % kP;
+      const int chl = chi[state * (m + 1) + s], chr = chi[state * (m + 1) + s + 1];
+      if (k < chl && r < chr) v = sites[state * stride + site_off[s] + (k * 2 + p) * chr + r];
+    }
+    out[idx] = v;
+  }
+}
+
+// per 32-state block and bond: max bond dim over the block
+__global__ void block_max_chi_kernel(const int32_t* __restrict__ chi, int m, int64_t n,
+                                     int64_t nblk, int32_t* __restrict__ out) {
+  const int64_t total = nblk * (m + 1);
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t blk = idx / (m + 1);
+    const int b = (int)(idx % (m + 1));
+    int mx = 1;
+    for (int l = 0; l < kLanes; ++l) {
+      const int64_t s = blk * kLanes + l;
+      if (s < n) mx = max(mx, chi[s * (m + 1) + b]);
+    }
+    out[idx] = mx;
+  }
+}
+
+__device__ __forceinline__ void store_result(int out_mode, double* out, int64_t ld, int64_t i,
+                                             int64_t j, double2 ov, bool mirror) {
+  if (out_mode == MPSKQ_OUT_KERNEL) {
+    const double h = hypot(ov.x, ov.y);  // abs(complex) ** 2 (kernel.py:174)
+    const double v = h * h;
+    out[i * ld + j] = v;
+    if (mirror) out[j * ld + i] = v;
+  } else {
+    reinterpret_cast<double2*>(out)[i * ld + j] = ov;
+    if (mirror) reinterpret_cast<double2*>(out)[j * ld + i] = cconj(ov);
+  }
+}
+
+// --------------------------------------------------------------- small chi
+struct O1Args {
+  const double2* bra;  // packed
+  const double2* ket;  // packed
+  const int32_t* bra_chi;
+  const int32_t* ket_bmax;
+  int64_t n_bras, n_kets, nblk_bra, nblk_ket;
+  int m, kind, out_mode;
+  const int2* tiles;  // (bra tile, ket block)
+  int64_t n_tiles;
+  double* out;
+  int64_t ld;
+};
+
+__global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) {
+  __shared__ double2 sA[kWarpsO1][kEnt];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = a.m;
+  for (int64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
+    const int2 tile = a.tiles[t];
+    const int64_t i = (int64_t)tile.x * kWarpsO1 + warp;  // bra (warp-uniform)
+    const int64_t j = (int64_t)tile.y * kLanes + lane;    // ket (per lane)
+    const int64_t ic = i < a.n_bras ? i : a.n_bras - 1;
+    const int32_t* bchi = a.bra_chi + ic * (m + 1);
+    const int32_t* kmax = a.ket_bmax + (int64_t)tile.y * (m + 1);
+    const int64_t ib = ic / kLanes, il = ic % kLanes;
+
+    double2 env[kP][kP];
+#pragma unroll
+    for (int x = 0; x < kP; ++x)
+#pragma unroll
+      for (int y = 0; y < kP; ++y) env[x][y] = make_double2(x == 0 && y == 0 ? 1.0 : 0.0, 0.0);
+
+    int na = 1, nb = 1;  // chi_s of bra / ket block
+    for (int s = 0; s < m; ++s) {
+      const int na1 = __ldg(bchi + s + 1);
+      const int nb1 = __ldg(kmax + s + 1);
+      // stage this warp's bra tensor (conjugated on use) in shared memory
+      sA[warp][lane] =
+          __ldg(a.bra + (((int64_t)s * a.nblk_bra + ib) * kEnt + lane) * kLanes + il);
+      __syncwarp();
+      const double2* kp = a.ket + (((int64_t)s * a.nblk_ket + tile.y) * kEnt) * kLanes + lane;
+      double2 nenv[kP][kP];
+#pragma unroll
+      for (int x = 0; x < kP; ++x)
+#pragma unroll
+        for (int y = 0; y < kP; ++y) nenv[x][y] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int br = 0; br < kP; ++br) {
+        if (br < nb1) {
+          // column br of the ket tensor: B[kb][p][br]
+          double2 Bc[kP][2];
+#pragma unroll
+          for (int kb = 0; kb < kP; ++kb)
+#pragma unroll
+            for (int p = 0; p < 2; ++p)
+              Bc[kb][p] = kb < nb ? __ldg(kp + ((kb * 2 + p) * kP + br) * kLanes)
+                                  : make_double2(0.0, 0.0);
+          // T[al][p] = sum_kb env[al][kb] B[kb][p][br]
+          double2 T[kP][2];
+#pragma unroll
+          for (int al = 0; al < kP; ++al) {
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+              double2 acc = make_double2(0.0, 0.0);
+              if (al < na) {
+#pragma unroll
+                for (int kb = 0; kb < kP; ++kb)
+                  if (kb < nb) acc = cfma(env[al][kb], Bc[kb][p], acc);
+              }
+              T[al][p] = acc;
+            }
+          }
+          // nenv[ar][br] = sum_{al,p} conj(A[al][p][ar]) T[al][p]
+#pragma unroll
+          for (int ar = 0; ar < kP; ++ar) {
+            if (ar < na1) {
+              double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+              for (int al = 0; al < kP; ++al) {
+                if (al < na) {
+#pragma unroll
+                  for (int p = 0; p < 2; ++p)
+                    acc = cfmac(sA[warp][(al * 2 + p) * kP + ar], T[al][p], acc);
+                }
+              }
+              nenv[ar][br] = acc;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int x = 0; x < kP; ++x)
+#pragma unroll
+        for (int y = 0; y < kP; ++y) env[x][y] = nenv[x][y];
+      na = na1;
+      nb = nb1;
+      __syncwarp();
+    }
+    const bool train = a.kind == MPSKQ_KIND_TRAIN;
+    const bool valid = i < a.n_bras && j < a.n_kets && (!train || i < j);
+    if (valid) store_result(a.out_mode, a.out, a.ld, i, j, env[0][0], train);
+  }
+}
+
+// --------------------------------------------------------------- generic chi
+template <int CAP>
+struct O2Cfg {
+  static constexpr int warps = CAP <= 8 ? 8 : CAP <= 16 ? 4 : 2;
+  static constexpr int nt = warps * 32;
+  static size_t smem() {
+    return sizeof(double2) * (2 * CAP * CAP + warps * (CAP * CAP + 2 * CAP * CAP));
+  }
+};
+
+struct O2Args {
+  const double2* bra;
+  const double2* ket;
+  const int32_t* bra_chi;
+  const int32_t* ket_chi;
+  const int64_t* site_off;
+  int64_t stride, n_bras, n_kets;
+  int m, kind, out_mode;
+  const int2* tiles;  // (bra, ket block)
+  int64_t n_tiles;
+  double* out;
+  int64_t ld;
+};
+
+template <int CAP>
+__global__ void __launch_bounds__(O2Cfg<CAP>::nt) overlap_o2_kernel(O2Args a) {
+  constexpr int NW = O2Cfg<CAP>::warps, NT = NW * 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* As = reinterpret_cast<double2*>(smem_raw);  // [al][p][ar] conj
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* env = As + 2 * CAP * CAP + warp * (3 * CAP * CAP);  // [al][kb], ld CAP
+  double2* T = env + CAP * CAP;                                 // [(al,p)][br], ld CAP
+  const int m = a.m;
+  const bool train = a.kind == MPSKQ_KIND_TRAIN;
+  for (int64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
+    const int2 tile = a.tiles[t];
+    const int64_t i = tile.x;
+    const int64_t j = (int64_t)tile.y * NW + warp;
+    const bool valid = j < a.n_kets && (!train || i < j);
+    const int64_t jc = j < a.n_kets ? j : a.n_kets - 1;
+    const double2* bra = a.bra + i * a.stride;
+    const double2* ket = a.ket + jc * a.stride;
+    const int32_t* bchi = a.bra_chi + i * (m + 1);
+    const int32_t* kchi = a.ket_chi + jc * (m + 1);
+    if (lane == 0) env[0] = make_double2(1.0, 0.0);
+    __syncwarp();
+    for (int s = 0; s < m; ++s) {
+      const int na = bchi[s], na1 = bchi[s + 1];
+      const int nb = kchi[s], nb1 = kchi[s + 1];
+      const double2* A = bra + a.site_off[s];
+      for (int idx = threadIdx.x; idx < na * 2 * na1; idx += NT) As[idx] = __ldg(A + idx);
+      __syncthreads();
+      const double2* B = ket + a.site_off[s];
+      // T[al][p][br] = sum_kb env[al][kb] B[kb][p][br]
+      for (int it = lane; it < na * 2 * nb1; it += 32) {
+        const int al = it / (2 * nb1), rem = it - al * 2 * nb1;
+        const int p = rem / nb1, br = rem - p * nb1;
+        double2 acc = cz();
+        for (int kb = 0; kb < nb; ++kb)
+          acc = cfma(env[al * CAP + kb], __ldg(B + (kb * 2 + p) * nb1 + br), acc);
+        T[(al * 2 + p) * CAP + br] = acc;
+      }
+      __syncwarp();
+      // env[ar][br] = sum_{al,p} conj(A[al][p][ar]) T[al][p][br]
+      for (int it = lane; it < na1 * nb1; it += 32) {
+        const int ar = it / nb1, br = it - ar * nb1;
+        double2 acc = cz();
+        for (int q = 0; q < 2 * na; ++q) acc = cfmac(As[q * na1 + ar], T[q * CAP + br], acc);
+        env[ar * CAP + br] = acc;
+      }
+      __syncwarp();
+      __syncthreads();
+    }
+    if (valid) store_result(a.out_mode, a.out, a.ld, i, j, env[0], train);
+    __syncwarp();
+  }
+}
+
+__global__ void fill_diag_kernel(double* out, int64_t ld, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i * ld + i] = 1.0;
+}
+
+int upload_tiles(const std::vector<int2>& tiles, int2** dev, cudaStream_t st) {
+  const size_t bytes = sizeof(int2) * (tiles.empty() ? 1 : tiles.size());
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(dev), bytes, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(tiles)");
+  if (!tiles.empty()) {
+    e = cudaMemcpyAsync(*dev, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(tiles)");
+  }
+  return MPSKQ_OK;
+}
+
+// tiles of (row block of rb rows, column block of cb columns); train keeps
+// the tiles holding some i < j.  Block-cyclic: tile t goes to rank t % world.
+std::vector<int2> make_tiles(bool train, int64_t n_rows, int64_t n_cols, int rb, int cb, int rank,
+                             int world) {
+  std::vector<int2> tiles;
+  const int64_t nrb = (n_rows + rb - 1) / rb, ncb = (n_cols + cb - 1) / cb;
+  int64_t t = 0;
+  for (int64_t J = 0; J < ncb; ++J) {
+    const int64_t jmax = std::min(n_cols, (J + 1) * cb) - 1;
+    for (int64_t I = 0; I < nrb; ++I) {
+      if (train && I * rb >= jmax) break;
+      if (t++ % world == rank) tiles.push_back(make_int2((int)I, (int)J));
+    }
+  }
+  return tiles;
+}
+
+int grid_for(int64_t n_tiles, int per_sm) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t cap = (int64_t)sms * per_sm * 64;
+  return (int)std::max<int64_t>(1, std::min(n_tiles, cap));
+}
+
+int launch_o1(const OverlapArgs& a, cudaStream_t st) {
+  const int m = a.m;
+  const bool same = a.bra_sites == a.ket_sites;
+  const int64_t nbb = (a.n_bras + kLanes - 1) / kLanes, nbk = (a.n_kets + kLanes - 1) / kLanes;
+  const size_t pb = sizeof(double2) * (size_t)m * nbb * kEnt * kLanes;
+  const size_t pk = sizeof(double2) * (size_t)m * nbk * kEnt * kLanes;
+  void *bra = nullptr, *ket = nullptr, *kmax = nullptr;
+  cudaError_t e = cudaMallocAsync(&bra, pb, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(packed bras)");
+  if (!same) {
+    e = cudaMallocAsync(&ket, pk, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(packed kets)");
+  } else {
+    ket = bra;
+  }
+  e = cudaMallocAsync(&kmax, sizeof(int32_t) * nbk * (m + 1), st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(block chi)");
+  const int threads = 256;
+  auto pack = [&](const double* sites, const int32_t* chi, int64_t n, int64_t nblk, void* out) {
+    const int64_t total = (int64_t)m * nblk * kEnt * kLanes;
+    const int blocks = (int)std::min<int64_t>((total + threads - 1) / threads, 148 * 64);
+    pack_o1_kernel<<<blocks, threads, 0, st>>>(reinterpret_cast<const double2*>(sites), chi,
+                                               a.site_off, a.state_stride, m, n, nblk,
+                                               static_cast<double2*>(out));
+  };
+  pack(a.bra_sites, a.bra_chi, a.n_bras, nbb, bra);
+  if (!same) pack(a.ket_sites, a.ket_chi, a.n_kets, nbk, ket);
+  {
+    const int64_t total = nbk * (m + 1);
+    const int blocks = (int)std::min<int64_t>((total + threads - 1) / threads, 148 * 16);
+    block_max_chi_kernel<<<blocks, threads, 0, st>>>(a.ket_chi, m, a.n_kets, nbk,
+                                                     static_cast<int32_t*>(kmax));
+  }
+  const bool train = a.kind == MPSKQ_KIND_TRAIN;
+  auto tiles = make_tiles(train, a.n_bras, a.n_kets, kWarpsO1, kLanes, a.rank, a.world);
+  int2* dtiles = nullptr;
+  if (int s = upload_tiles(tiles, &dtiles, st)) return s;
+  if (!tiles.empty()) {
+    O1Args o{static_cast<const double2*>(bra), static_cast<const double2*>(ket), a.bra_chi,
+             static_cast<const int32_t*>(kmax), a.n_bras, a.n_kets, nbb, nbk, m, a.kind,
+             a.out_mode, dtiles, (int64_t)tiles.size(), a.out, a.ld};
+    overlap_o1_kernel<<<grid_for((int64_t)tiles.size(), 1), kWarpsO1 * 32, 0, st>>>(o);
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "overlap_o1 launch");
+  cudaFreeAsync(dtiles, st);
+  cudaFreeAsync(kmax, st);
+  if (!same) cudaFreeAsync(ket, st);
+  cudaFreeAsync(bra, st);
+  return MPSKQ_OK;
+}
+
+template <int CAP>
+int launch_o2(const OverlapArgs& a, cudaStream_t st) {
+  using C = O2Cfg<CAP>;
+  const size_t smem = C::smem();
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(overlap_o2_kernel<CAP>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(o2)");
+  }
+  const bool train = a.kind == MPSKQ_KIND_TRAIN;
+  auto tiles = make_tiles(train, a.n_bras, a.n_kets, 1, C::warps, a.rank, a.world);
+  int2* dtiles = nullptr;
+  if (int s = upload_tiles(tiles, &dtiles, st)) return s;
+  if (!tiles.empty()) {
+    O2Args o{reinterpret_cast<const double2*>(a.bra_sites),
+             reinterpret_cast<const double2*>(a.ket_sites),
+             a.bra_chi,
+             a.ket_chi,
+             a.site_off,
+             a.state_stride,
+             a.n_bras,
+             a.n_kets,
+             a.m,
+             a.kind,
+             a.out_mode,
+             dtiles,
+             (int64_t)tiles.size(),
+             a.out,
+             a.ld};
+    overlap_o2_kernel<CAP><<<grid_for((int64_t)tiles.size(), 4), C::nt, smem, st>>>(o);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "overlap_o2 launch");
+  cudaFreeAsync(dtiles, st);
+  return MPSKQ_OK;
+}
+
+}  // namespace
+
+int launch_overlap(const OverlapArgs& a, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int s = MPSKQ_OK;
+  switch (a.chi_cap) {
+    case 4: s = launch_o1(a, st); break;
+    case 8: s = launch_o2<8>(a, st); break;
+    case 16: s = launch_o2<16>(a, st); break;
+    case 32: s = launch_o2<32>(a, st); break;
+    default: return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", a.chi_cap);
+  }
+  if (s != MPSKQ_OK) return s;
+  if (a.kind == MPSKQ_KIND_TRAIN && a.out_mode == MPSKQ_OUT_KERNEL && a.rank == 0) {
+    fill_diag_kernel<<<(int)std::min<int64_t>((a.n_bras + 255) / 256, 1024), 256, 0, st>>>(
+        a.out, a.ld, a.n_bras);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "fill_diag launch");
+  }
+  return MPSKQ_OK;
+}
+
+void tile_shape(int chi_cap, int* rb, int* cb) {
+  switch (chi_cap) {
+    case 4: *rb = kWarpsO1; *cb = kLanes; return;
+    case 8: *rb = 1; *cb = O2Cfg<8>::warps; return;
+    case 16: *rb = 1; *cb = O2Cfg<16>::warps; return;
+    default: *rb = 1; *cb = O2Cfg<32>::warps; return;
+  }
+}
+
+}  // namespace mpskq
+
+extern "C" int mpskq_overlap_tiles(int kind, int chi_cap, int64_t n_bras, int64_t n_kets, int rank,
+                                   int world, int32_t* tiles, int64_t cap, int64_t* n_tiles,
+                                   int32_t* row_block, int32_t* col_block) {
+  using namespace mpskq;
+  if (kind != MPSKQ_KIND_TRAIN && kind != MPSKQ_KIND_TEST)
+    return fail(MPSKQ_ERR_INVALID, "kind must be one of ('train', 'test')");
+  if (!chi_cap_supported(chi_cap))
+    return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", chi_cap);
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(MPSKQ_ERR_INVALID, "bad rank %d of world %d", rank, world);
+  if (n_bras < 0 || n_kets < 0) return fail(MPSKQ_ERR_INVALID, "negative state counts");
+  int rb = 1, cb = 1;
+  tile_shape(chi_cap, &rb, &cb);
+  if (row_block) *row_block = rb;
+  if (col_block) *col_block = cb;
+  auto t = make_tiles(kind == MPSKQ_KIND_TRAIN, n_bras, n_kets, rb, cb, rank, world);
+  if (n_tiles) *n_tiles = (int64_t)t.size();
+  if (!tiles) return MPSKQ_OK;
+  if (cap < (int64_t)t.size()) return fail(MPSKQ_ERR_INVALID, "tile buffer too small");
+  for (size_t i = 0; i < t.size(); ++i) {
+    tiles[2 * i] = t[i].x;
+    tiles[2 * i + 1] = t[i].y;
+  }
+  return MPSKQ_OK;
+}

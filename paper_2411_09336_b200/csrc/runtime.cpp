@@ -1,0 +1,602 @@
+// Host runtime of libmpskq: error state, feature-map topology, angle and
+// coefficient encoding, program compiler, batch layout and the end-to-end
+// host-buffer pipeline.  Device work lives in sim.cu / overlap.cu.
+//
+// Reference citations are /root/reference/pkg/src/mpskernel/<file>:<line>.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+#include "internal.h"
+
+namespace mpskq {
+
+static thread_local char g_err[1024] = "";
+
+int fail(int status, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return status;
+}
+
+int cuda_fail(int err, const char* what) {
+  return fail(MPSKQ_ERR_CUDA, "%s: %s", what, cudaGetErrorString((cudaError_t)err));
+}
+
+int64_t bond_cap(int m, int chi_cap, int b) {
+  int e = std::min(b, m - b);
+  if (e >= 30) return chi_cap;
+  return std::min<int64_t>(chi_cap, int64_t(1) << e);
+}
+
+namespace {
+
+struct Gate {
+  int kind, a, b, slot;
+};
+
+// interaction_graph (ansatz.py:102-106): edges grouped by distance k, then i
+std::vector<std::pair<int, int>> edges_of(int m, int d) {
+  std::vector<std::pair<int, int>> e;
+  for (int k = 1; k <= d; ++k)
+    for (int i = 0; i + k < m; ++i) e.emplace_back(i, i + k);
+  return e;
+}
+
+int check_cfg(int m, int r, int d) {
+  // FeatureMapConfig.__post_init__ (ansatz.py:33-41)
+  if (m < 1) return fail(MPSKQ_ERR_INVALID, "m must be at least 1");
+  if (r < 1) return fail(MPSKQ_ERR_INVALID, "r must be at least 1");
+  if (!(1 <= d && d <= m - 1))
+    return fail(MPSKQ_ERR_INVALID, "d must satisfy 1 <= d <= m-1, got d=%d for m=%d", d, m);
+  return MPSKQ_OK;
+}
+
+// greedy first-fit layering of one run of RXX gates (ansatz.py:139-161)
+void schedule_run(const std::vector<Gate>& run, int m, int d, std::vector<Gate>& out) {
+  std::vector<std::vector<Gate>> layers;
+  std::vector<std::vector<char>> used;
+  for (const Gate& g : run) {
+    bool placed = false;
+    for (size_t l = 0; l < layers.size(); ++l) {
+      if (!used[l][g.a] && !used[l][g.b]) {
+        layers[l].push_back(g);
+        used[l][g.a] = used[l][g.b] = 1;
+        placed = true;
+        break;
+      }
+    }
+    if (!placed) {
+      layers.push_back({g});
+      used.emplace_back(m, 0);
+      used.back()[g.a] = used.back()[g.b] = 1;
+    }
+  }
+  (void)d;  // the reference asserts len(layers) <= 2d; the banded graph guarantees it
+  for (auto& l : layers)
+    for (auto& g : l) out.push_back(g);
+}
+
+std::vector<Gate> feature_map_gates(int m, int r, int d, int64_t* n_params) {
+  auto edges = edges_of(m, d);
+  const int E = (int)edges.size();
+  // build_circuit (ansatz.py:126-136)
+  std::vector<Gate> built;
+  for (int q = 0; q < m; ++q) built.push_back({MPSKQ_GATE_H, q, -1, -1});
+  for (int l = 0; l < r; ++l) {
+    for (int q = 0; q < m; ++q) built.push_back({MPSKQ_GATE_RZ, q, -1, l * (m + E) + q});
+    for (int e = 0; e < E; ++e)
+      built.push_back({MPSKQ_GATE_RXX, edges[e].first, edges[e].second, l * (m + E) + m + e});
+  }
+  *n_params = (int64_t)r * (m + E);
+  // schedule_circuit (ansatz.py:170-184)
+  std::vector<Gate> sched, run;
+  for (const Gate& g : built) {
+    if (g.kind == MPSKQ_GATE_RXX) {
+      run.push_back(g);
+    } else {
+      if (!run.empty()) schedule_run(run, m, d, sched), run.clear();
+      sched.push_back(g);
+    }
+  }
+  if (!run.empty()) schedule_run(run, m, d, sched);
+  // route_linear (ansatz.py:187-215)
+  std::vector<int> pos(m), occ(m);
+  for (int i = 0; i < m; ++i) pos[i] = occ[i] = i;
+  std::vector<Gate> out;
+  auto emit_swap = [&](int p) {
+    out.push_back({MPSKQ_GATE_SWAP, p, p + 1, -1});
+    int la = occ[p], lb = occ[p + 1];
+    occ[p] = lb;
+    occ[p + 1] = la;
+    pos[la] = p + 1;
+    pos[lb] = p;
+  };
+  for (const Gate& g : sched) {
+    if (g.b < 0) {
+      out.push_back({g.kind, pos[g.a], -1, g.slot});
+      continue;
+    }
+    int lo = std::min(pos[g.a], pos[g.b]), hi = std::max(pos[g.a], pos[g.b]);
+    for (int p = hi - 1; p > lo; --p) emit_swap(p);
+    out.push_back({g.kind, lo, lo + 1, g.slot});
+    for (int p = lo + 1; p < hi; ++p) emit_swap(p);
+  }
+  return out;
+}
+
+}  // namespace
+}  // namespace mpskq
+
+using namespace mpskq;
+
+extern "C" {
+
+int mpskq_abi_version(void) { return MPSKQ_ABI_VERSION; }
+const char* mpskq_last_error(void) { return g_err; }
+
+int mpskq_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int mpskq_feature_map_topology(int m, int r, int d, int32_t* kinds, int32_t* q0, int32_t* q1,
+                               int32_t* param_slot, int64_t cap, int64_t* n_gates,
+                               int64_t* n_params) {
+  if (int st = check_cfg(m, r, d)) return st;
+  int64_t np = 0;
+  auto gates = feature_map_gates(m, r, d, &np);
+  if (n_gates) *n_gates = (int64_t)gates.size();
+  if (n_params) *n_params = np;
+  if (!kinds) return MPSKQ_OK;
+  if (cap < (int64_t)gates.size())
+    return fail(MPSKQ_ERR_INVALID, "topology needs %zu gates, buffer holds %lld", gates.size(),
+                (long long)cap);
+  for (size_t i = 0; i < gates.size(); ++i) {
+    kinds[i] = gates[i].kind;
+    q0[i] = gates[i].a;
+    q1[i] = gates[i].b;
+    param_slot[i] = gates[i].slot;
+  }
+  return MPSKQ_OK;
+}
+
+int mpskq_feature_map_angles(const double* X, int64_t n_rows, int m, int r, int d, double gamma,
+                             double* angles) {
+  if (int st = check_cfg(m, r, d)) return st;
+  if (!(gamma > 0)) return fail(MPSKQ_ERR_INVALID, "gamma must be positive");
+  if (n_rows < 0) return fail(MPSKQ_ERR_INVALID, "negative row count");
+  auto edges = edges_of(m, d);
+  const int64_t E = (int64_t)edges.size(), np = (int64_t)r * (m + E);
+  // the reference's expression order, ansatz.py:130 and :132; gamma**2 is
+  // pow(gamma, 2) which is the correctly rounded gamma*gamma
+  const double g2 = gamma * gamma;
+  const double rz_scale = 2.0 * gamma;
+  const double rxx_scale = (2.0 * g2) * (M_PI / 2.0);
+  for (int64_t n = 0; n < n_rows; ++n) {
+    const double* x = X + n * m;
+    for (int q = 0; q < m; ++q) {
+      if (!std::isfinite(x[q])) return fail(MPSKQ_ERR_INVALID, "features must be finite");
+      if (x[q] < 0.0 || x[q] > 2.0)
+        return fail(MPSKQ_ERR_INVALID, "features must lie in [0, 2]; rescale the data first");
+    }
+    double* out = angles + n * np;
+    for (int l = 0; l < r; ++l) {
+      double* o = out + (int64_t)l * (m + E);
+      for (int q = 0; q < m; ++q) o[q] = rz_scale * x[q];
+      for (int64_t e = 0; e < E; ++e) {
+        const int i = edges[e].first, j = edges[e].second;
+        double a = rxx_scale * (1.0 - x[i]);
+        o[m + e] = a * (1.0 - x[j]);
+      }
+    }
+  }
+  return MPSKQ_OK;
+}
+
+int mpskq_feature_map_coefficients_device(const double* X_dev, int64_t n_rows, int m, int r,
+                                          int d, double gamma, double* coef_dev, int* bad_dev,
+                                          void* stream) {
+  if (int st = check_cfg(m, r, d)) return st;
+  if (!(gamma > 0)) return fail(MPSKQ_ERR_INVALID, "gamma must be positive");
+  if (n_rows < 0) return fail(MPSKQ_ERR_INVALID, "negative row count");
+  return launch_encode(X_dev, n_rows, m, r, d, gamma, coef_dev, bad_dev, stream);
+}
+
+int mpskq_half_angle_coefficients(const double* angles, int64_t n, double* coef) {
+  for (int64_t i = 0; i < n; ++i) {
+    const double half = 0.5 * angles[i];  // gate_matrix, ansatz.py:92
+    coef[2 * i] = std::cos(half);
+    coef[2 * i + 1] = std::sin(half);
+  }
+  return MPSKQ_OK;
+}
+
+int mpskq_program_compile(int m, int64_t n_gates, const int32_t* kinds, const int32_t* q0,
+                          const int32_t* q1, const int32_t* param_slot, int32_t* ops,
+                          int64_t cap_ops, int64_t* n_ops, int64_t* n_qr_left,
+                          int64_t* n_qr_right) {
+  if (m < 1) return fail(MPSKQ_ERR_INVALID, "qubit count must be at least 1");
+  // next two-qubit gate's lower qubit after each index (run_circuit, mps.py:233-236)
+  std::vector<int> next2(n_gates + 1, -1);
+  for (int64_t i = n_gates - 1; i >= 0; --i) {
+    const bool two = kinds[i] == MPSKQ_GATE_RXX || kinds[i] == MPSKQ_GATE_SWAP;
+    next2[i] = two ? std::min(q0[i], q1[i]) : next2[i + 1];
+  }
+  int64_t count = 0, nl = 0, nr = 0;
+  auto emit = [&](int code, int site, int slot, int gidx) {
+    if (ops) {
+      if (count >= cap_ops) return false;
+      ops[4 * count + 0] = code;
+      ops[4 * count + 1] = site;
+      ops[4 * count + 2] = slot;
+      ops[4 * count + 3] = gidx;
+    }
+    ++count;
+    return true;
+  };
+  int center = 0;  // init_state: ortho_center = 0 (mps.py:102)
+  for (int64_t i = 0; i < n_gates; ++i) {
+    const int k = kinds[i];
+    if (k < MPSKQ_GATE_H || k > MPSKQ_GATE_SWAP)
+      return fail(MPSKQ_ERR_INVALID, "unknown gate kind %d", k);
+    const bool two = k == MPSKQ_GATE_RXX || k == MPSKQ_GATE_SWAP;
+    const bool param = k == MPSKQ_GATE_RZ || k == MPSKQ_GATE_RXX;
+    if (param && param_slot[i] < 0)
+      return fail(MPSKQ_ERR_INVALID, "gate %lld requires an angle", (long long)i);
+    if (!two) {
+      if (q0[i] < 0 || q0[i] >= m)
+        return fail(MPSKQ_ERR_INVALID, "qubit %d out of range for %d sites", q0[i], m);
+      if (!emit(k == MPSKQ_GATE_H ? MPSKQ_OP_H : MPSKQ_OP_RZ, q0[i], param ? param_slot[i] : -1,
+                (int)i))
+        return fail(MPSKQ_ERR_INVALID, "op buffer too small");
+      continue;
+    }
+    const int a = q0[i], b = q1[i];
+    if (a < 0 || a >= m || b < 0 || b >= m)
+      return fail(MPSKQ_ERR_INVALID, "qubit out of range for %d sites", m);
+    if (std::abs(a - b) != 1)
+      return fail(MPSKQ_ERR_INVALID,
+                  "two-qubit gate on (%d, %d) is not adjacent; route the circuit first", a, b);
+    // H, RZ, RXX and SWAP are all symmetric under exchanging the two qubits,
+    // so apply_gate's transpose for a > b (mps.py:219-220) is the identity.
+    const int q = std::min(a, b);
+    const int nxt = next2[i + 1];
+    const bool left = nxt >= 0 && nxt <= q;
+    // canonicalize(state, q) (mps.py:123-138)
+    if (center < q) {
+      for (int s = center; s < q; ++s, ++nl)
+        if (!emit(MPSKQ_OP_QRL, s, -1, -1)) return fail(MPSKQ_ERR_INVALID, "op buffer too small");
+    } else if (center > q) {
+      for (int s = center; s > q; --s, ++nr)
+        if (!emit(MPSKQ_OP_QRR, s, -1, -1)) return fail(MPSKQ_ERR_INVALID, "op buffer too small");
+    }
+    const int code = (k == MPSKQ_GATE_RXX ? MPSKQ_OP_RXX : MPSKQ_OP_SWAP) |
+                     ((left ? MPSKQ_ABSORB_LEFT : 0) << 8);
+    if (!emit(code, q, param ? param_slot[i] : -1, (int)i))
+      return fail(MPSKQ_ERR_INVALID, "op buffer too small");
+    center = left ? q : q + 1;
+  }
+  if (n_ops) *n_ops = count;
+  if (n_qr_left) *n_qr_left = nl;
+  if (n_qr_right) *n_qr_right = nr;
+  return MPSKQ_OK;
+}
+
+int mpskq_batch_layout(int m, int chi_cap, int64_t* site_off, int64_t* state_stride) {
+  if (m < 1) return fail(MPSKQ_ERR_INVALID, "qubit count must be at least 1");
+  if (!chi_cap_supported(chi_cap))
+    return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", chi_cap);
+  int64_t off = 0;
+  for (int s = 0; s < m; ++s) {
+    if (site_off) site_off[s] = off;
+    off += 2 * bond_cap(m, chi_cap, s) * bond_cap(m, chi_cap, s + 1);
+  }
+  off = (off + 1) & ~int64_t(1);  // keep every state 32-byte aligned
+  if (site_off) site_off[m] = off;
+  if (state_stride) *state_stride = off;
+  return MPSKQ_OK;
+}
+
+int mpskq_supported_chi_caps(int32_t* caps, int cap, int* n) {
+  if (n) *n = kNumChiCaps;
+  for (int i = 0; i < kNumChiCaps && i < cap; ++i) caps[i] = kChiCaps[i];
+  return MPSKQ_OK;
+}
+
+int mpskq_simulate(int m, int chi_cap, const int32_t* ops_dev, int64_t n_ops, int64_t n_gates,
+                   const double* coef_dev, int64_t n_params, int64_t n_states, double budget,
+                   int chi_max, const int64_t* site_off_dev, int64_t state_stride,
+                   double* sites_dev, int32_t* chi_dev, double* discard_dev,
+                   int32_t* peak_chi_dev, int32_t* status_dev, int64_t* entry_log_dev,
+                   void* stream) {
+  if (m < 1) return fail(MPSKQ_ERR_INVALID, "qubit count must be at least 1");
+  if (!chi_cap_supported(chi_cap))
+    return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", chi_cap);
+  if (!(budget >= 0)) return fail(MPSKQ_ERR_INVALID, "budget must be non-negative");
+  if (n_states < 0 || n_ops < 0) return fail(MPSKQ_ERR_INVALID, "negative sizes");
+  if (n_states == 0) return MPSKQ_OK;
+  SimArgs a{m,        chi_cap,  ops_dev,      n_ops,        n_gates,   coef_dev,
+            n_params, n_states, budget,       chi_max,      site_off_dev, state_stride,
+            sites_dev, chi_dev, discard_dev,  peak_chi_dev, status_dev, entry_log_dev};
+  return launch_simulate(a, stream);
+}
+
+int mpskq_svd_truncated_batched(int rows, int cols, int64_t batch, const double* mats_dev,
+                                double budget, int chi_max, double* u_dev, double* s_dev,
+                                double* vh_dev, int32_t* keep_dev, double* discarded_dev,
+                                int32_t* status_dev, void* stream) {
+  if (rows < 1 || cols < 1)
+    return fail(MPSKQ_ERR_INVALID, "split must leave a non-empty axis group on each side");
+  if (!(budget >= 0)) return fail(MPSKQ_ERR_INVALID, "budget must be non-negative");
+  const int maxdim = 2 * kChiCaps[kNumChiCaps - 1];
+  if (rows > maxdim || cols > maxdim)
+    return fail(MPSKQ_ERR_INVALID, "matrix %dx%d exceeds the %dx%d device SVD envelope", rows,
+                cols, maxdim, maxdim);
+  if (batch <= 0) return MPSKQ_OK;
+  SvdArgs a{rows, cols, batch, mats_dev, budget, chi_max, u_dev, s_dev, vh_dev, keep_dev,
+            discarded_dev, status_dev};
+  return launch_svd(a, stream);
+}
+
+int mpskq_overlap(int kind, int out_mode, int m, int chi_cap, const int64_t* site_off_dev,
+                  int64_t state_stride, const double* bra_sites_dev, const int32_t* bra_chi_dev,
+                  int64_t n_bras, const double* ket_sites_dev, const int32_t* ket_chi_dev,
+                  int64_t n_kets, int rank, int world, double* out_dev, int64_t ld,
+                  void* stream) {
+  if (kind != MPSKQ_KIND_TRAIN && kind != MPSKQ_KIND_TEST)
+    return fail(MPSKQ_ERR_INVALID, "kind must be one of ('train', 'test')");
+  if (out_mode != MPSKQ_OUT_KERNEL && out_mode != MPSKQ_OUT_AMPLITUDE)
+    return fail(MPSKQ_ERR_INVALID, "unknown output mode %d", out_mode);
+  if (!chi_cap_supported(chi_cap))
+    return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", chi_cap);
+  if (kind == MPSKQ_KIND_TRAIN &&
+      (n_bras != n_kets || bra_sites_dev != ket_sites_dev || bra_chi_dev != ket_chi_dev))
+    return fail(MPSKQ_ERR_INVALID, "train kind requires bras and kets to be the same states");
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(MPSKQ_ERR_INVALID, "bad rank %d of world %d", rank, world);
+  if (ld < n_kets) return fail(MPSKQ_ERR_INVALID, "leading dimension smaller than ket count");
+  if (n_bras == 0 || n_kets == 0) return MPSKQ_OK;
+  OverlapArgs a{kind,     out_mode,      m,        chi_cap,       site_off_dev, state_stride,
+                bra_sites_dev, bra_chi_dev, n_bras, ket_sites_dev, ket_chi_dev,  n_kets,
+                rank,     world,         out_dev,  ld};
+  return launch_overlap(a, stream);
+}
+
+int mpskq_fp64_probe(int n_blocks, int64_t iters, double* out_dev, void* stream) {
+  if (n_blocks < 1 || iters < 1) return fail(MPSKQ_ERR_INVALID, "bad probe size");
+  return launch_fp64_probe(n_blocks, iters, out_dev, stream);
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ end to end
+namespace {
+
+// stream-ordered device allocation (pool-backed, cheap after warm-up)
+struct AsyncBuf {
+  void* p = nullptr;
+  cudaStream_t st = nullptr;
+  AsyncBuf() = default;
+  AsyncBuf(const AsyncBuf&) = delete;
+  AsyncBuf& operator=(const AsyncBuf&) = delete;
+  ~AsyncBuf() { reset(); }
+  void reset() {
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+  }
+  int alloc(size_t bytes, cudaStream_t s) {
+    st = s;
+    cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 8, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+    return MPSKQ_OK;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct ProgramCache {
+  std::mutex mu;
+  std::map<std::tuple<int, int, int>, std::pair<std::vector<int32_t>, int64_t>> progs;  // ops, n_gates
+  std::map<std::tuple<int, int, int, double, int>, int> cap_hint;
+};
+ProgramCache& cache() {
+  static ProgramCache c;
+  return c;
+}
+
+int program_for(int m, int r, int d, std::vector<int32_t>& ops, int64_t& n_gates) {
+  {
+    std::lock_guard<std::mutex> g(cache().mu);
+    auto it = cache().progs.find({m, r, d});
+    if (it != cache().progs.end()) {
+      ops = it->second.first;
+      n_gates = it->second.second;
+      return MPSKQ_OK;
+    }
+  }
+  int64_t n_params = 0, n_ops = 0;
+  int st = mpskq_feature_map_topology(m, r, d, nullptr, nullptr, nullptr, nullptr, 0, &n_gates, &n_params);
+  if (st) return st;
+  std::vector<int32_t> kinds(n_gates), q0(n_gates), q1(n_gates), slot(n_gates);
+  st = mpskq_feature_map_topology(m, r, d, kinds.data(), q0.data(), q1.data(), slot.data(), n_gates,
+                                  &n_gates, &n_params);
+  if (st) return st;
+  st = mpskq_program_compile(m, n_gates, kinds.data(), q0.data(), q1.data(), slot.data(), nullptr, 0,
+                             &n_ops, nullptr, nullptr);
+  if (st) return st;
+  ops.assign(4 * n_ops, 0);
+  st = mpskq_program_compile(m, n_gates, kinds.data(), q0.data(), q1.data(), slot.data(), ops.data(),
+                             n_ops, &n_ops, nullptr, nullptr);
+  if (st) return st;
+  std::lock_guard<std::mutex> g(cache().mu);
+  cache().progs[{m, r, d}] = {ops, n_gates};
+  return MPSKQ_OK;
+}
+
+#define CK(expr)                                        \
+  do {                                                  \
+    cudaError_t e_ = (expr);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #expr); \
+  } while (0)
+#define ST(expr)                \
+  do {                          \
+    int s_ = (expr);            \
+    if (s_ != MPSKQ_OK) return s_; \
+  } while (0)
+
+int check_rows_host(const double* X, int64_t n, int m) {
+  for (int64_t i = 0; i < n * m; ++i) {
+    if (!std::isfinite(X[i])) return fail(MPSKQ_ERR_INVALID, "features must be finite");
+    if (X[i] < 0.0 || X[i] > 2.0)
+      return fail(MPSKQ_ERR_INVALID, "features must lie in [0, 2]; rescale the data first");
+  }
+  return MPSKQ_OK;
+}
+
+}  // namespace
+
+extern "C" int mpskq_gram_host(int kind, int m, int r, int d, double gamma, double budget,
+                               int chi_max, int chi_cap, const double* X_bras, int64_t n_bras,
+                               const double* X_kets, int64_t n_kets, double* K_out, void* stream,
+                               double* seconds) {
+  if (kind != MPSKQ_KIND_TRAIN && kind != MPSKQ_KIND_TEST)
+    return fail(MPSKQ_ERR_INVALID, "kind must be one of ('train', 'test')");
+  ST(check_cfg(m, r, d));
+  if (!(gamma > 0)) return fail(MPSKQ_ERR_INVALID, "gamma must be positive");
+  if (!(budget >= 0)) return fail(MPSKQ_ERR_INVALID, "budget must be non-negative");
+  if (chi_cap != 0 && !chi_cap_supported(chi_cap))
+    return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", chi_cap);
+  const bool train = kind == MPSKQ_KIND_TRAIN;
+  if (train) {
+    X_kets = X_bras;
+    n_kets = n_bras;
+  }
+  if (n_bras < 0 || n_kets < 0) return fail(MPSKQ_ERR_INVALID, "negative row count");
+  ST(check_rows_host(X_bras, n_bras, m));
+  if (!train) ST(check_rows_host(X_kets, n_kets, m));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t n_all = train ? n_bras : n_bras + n_kets;
+
+  std::vector<int32_t> ops;
+  int64_t n_gates = 0;
+  ST(program_for(m, r, d, ops, n_gates));
+  const int64_t n_ops = (int64_t)ops.size() / 4;
+  int E = 0;
+  for (int k = 1; k <= d; ++k) E += m - k;
+  const int64_t n_params = (int64_t)r * (m + E);
+
+  cudaEvent_t ev[4];
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() {
+      for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]);
+    }
+  } evg{ev};
+
+  CK(cudaEventRecord(ev[0], st));
+  AsyncBuf dX, dcoef, dops, dbad;
+  ST(dX.alloc(sizeof(double) * n_all * m, st));
+  ST(dcoef.alloc(sizeof(double) * 2 * n_all * n_params, st));
+  ST(dops.alloc(sizeof(int32_t) * ops.size(), st));
+  ST(dbad.alloc(sizeof(int), st));
+  if (n_bras) CK(cudaMemcpyAsync(dX.p, X_bras, sizeof(double) * n_bras * m, cudaMemcpyHostToDevice, st));
+  if (!train && n_kets)
+    CK(cudaMemcpyAsync(dX.as<double>() + n_bras * m, X_kets, sizeof(double) * n_kets * m,
+                       cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dops.p, ops.data(), sizeof(int32_t) * ops.size(), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(dbad.p, 0, sizeof(int), st));
+  ST(launch_encode(dX.as<double>(), n_all, m, r, d, gamma, dcoef.as<double>(), dbad.as<int>(), st));
+
+  // simulate every state once, escalating the chi capacity on overflow
+  const auto key = std::make_tuple(m, r, d, budget, chi_max);
+  int cap_idx = 0;
+  if (chi_cap) {
+    while (kChiCaps[cap_idx] != chi_cap) ++cap_idx;
+  } else {
+    std::lock_guard<std::mutex> g(cache().mu);
+    auto it = cache().cap_hint.find(key);
+    if (it != cache().cap_hint.end()) cap_idx = it->second;
+  }
+  AsyncBuf sites, chi, disc, peak, status, doff;
+  int64_t stride = 0;
+  int cap = 0;
+  std::vector<int32_t> hstatus(n_all);
+  for (;; ++cap_idx) {
+    if (cap_idx >= kNumChiCaps)
+      return fail(MPSKQ_ERR_CAPACITY, "bond dimension exceeds the largest compiled capacity %d",
+                  kChiCaps[kNumChiCaps - 1]);
+    cap = kChiCaps[cap_idx];
+    std::vector<int64_t> off(m + 1);
+    ST(mpskq_batch_layout(m, cap, off.data(), &stride));
+    for (AsyncBuf* b : {&sites, &chi, &disc, &peak, &status, &doff}) b->reset();
+    ST(doff.alloc(sizeof(int64_t) * (m + 1), st));
+    CK(cudaMemcpyAsync(doff.p, off.data(), sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice, st));
+    ST(sites.alloc(sizeof(double) * 2 * stride * n_all, st));
+    ST(chi.alloc(sizeof(int32_t) * (m + 1) * n_all, st));
+    ST(disc.alloc(sizeof(double) * n_all, st));
+    ST(peak.alloc(sizeof(int32_t) * n_all, st));
+    ST(status.alloc(sizeof(int32_t) * n_all, st));
+    ST(mpskq_simulate(m, cap, dops.as<int32_t>(), n_ops, n_gates, dcoef.as<double>(), n_params, n_all,
+                      budget, chi_max, doff.as<int64_t>(), stride, sites.as<double>(),
+                      chi.as<int32_t>(), disc.as<double>(), peak.as<int32_t>(),
+                      status.as<int32_t>(), nullptr, stream));
+    CK(cudaMemcpyAsync(hstatus.data(), status.p, sizeof(int32_t) * n_all, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    bool overflow = false;
+    for (int32_t s : hstatus) {
+      if (s == MPSKQ_STATE_NONFINITE)
+        return fail(MPSKQ_ERR_NUMERIC, "tensor has non-finite entries");
+      overflow |= s == MPSKQ_STATE_CAPACITY;
+    }
+    if (!overflow) break;
+    if (chi_cap) return fail(MPSKQ_ERR_CAPACITY, "bond dimension exceeds chi capacity %d", cap);
+  }
+  if (!chi_cap) {
+    std::lock_guard<std::mutex> g(cache().mu);
+    cache().cap_hint[key] = cap_idx;
+  }
+  CK(cudaEventRecord(ev[1], st));
+
+  AsyncBuf dK;
+  ST(dK.alloc(sizeof(double) * n_bras * n_kets, st));
+  const double* bra_sites = sites.as<double>();
+  const int32_t* bra_chi = chi.as<int32_t>();
+  const double* ket_sites = train ? bra_sites : bra_sites + 2 * stride * n_bras;
+  const int32_t* ket_chi = train ? bra_chi : bra_chi + (m + 1) * n_bras;
+  ST(mpskq_overlap(kind, MPSKQ_OUT_KERNEL, m, cap, doff.as<int64_t>(), stride, bra_sites, bra_chi,
+                   n_bras, ket_sites, ket_chi, n_kets, 0, 1, dK.as<double>(), n_kets, stream));
+  CK(cudaEventRecord(ev[2], st));
+  if (n_bras * n_kets)
+    CK(cudaMemcpyAsync(K_out, dK.p, sizeof(double) * n_bras * n_kets, cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(ev[3], st));
+  CK(cudaStreamSynchronize(st));
+  if (seconds) {
+    float t01 = 0, t12 = 0, t23 = 0;
+    cudaEventElapsedTime(&t01, ev[0], ev[1]);
+    cudaEventElapsedTime(&t12, ev[1], ev[2]);
+    cudaEventElapsedTime(&t23, ev[2], ev[3]);
+    seconds[0] = 1e-3 * t01;
+    seconds[1] = 1e-3 * t12;
+    seconds[2] = 0.0;
+    seconds[3] = 1e-3 * t23;
+  }
+  return MPSKQ_OK;
+}

@@ -1,0 +1,393 @@
+"""MPS states and the GPU simulation / overlap entry points.
+
+Drop-in for the hot-path names of the reference's ``mpskernel.mps``
+(/root/reference/pkg/src/mpskernel/mps.py):
+
+* ``MpsState`` / ``SimStats`` / ``stats`` / ``init_state`` / ``to_statevector``
+  are host-side containers and helpers with the reference's fields.
+* ``simulate_circuit`` (mps.py:250-257) and ``inner_product`` (mps.py:260-268)
+  run on the GPU through libmpskq.
+* ``MpsBatch`` is the device-resident batch the GPU path produces: a
+  sequence whose items are ``MpsState`` views (copied to the host on access)
+  with site arrays in the reference layout.
+"""
+
+from __future__ import annotations
+
+import functools
+from collections.abc import Sequence
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from ._device import Timer, dptr, require_cuda, stream_ptr
+from .ansatz import Circuit, Topology, circuit_topology, half_angle_coefficients
+
+DEFAULT_TRUNC_BUDGET = 1e-24  # mps.py:25
+_MAX_DENSE_QUBITS = 20
+
+
+@dataclass
+class MpsState:
+    """Chain of (chi_l, 2, chi_r) site tensors plus truncation bookkeeping (mps.py:31-77)."""
+
+    sites: list
+    trunc_budget_per_gate: float = DEFAULT_TRUNC_BUDGET
+    accumulated_discard: float = 0.0
+    ortho_center: int | None = None
+    peak_chi: int = 1
+    gate_count_1q: int = 0
+    gate_count_2q: int = 0
+    timings: dict = field(default_factory=dict)
+
+    @property
+    def m(self) -> int:
+        return len(self.sites)
+
+    def bond_dims(self) -> list:
+        return [t.shape[0] for t in self.sites] + [self.sites[-1].shape[2]]
+
+    def max_bond(self) -> int:
+        return max(self.bond_dims())
+
+    def entry_count(self) -> int:
+        return sum(t.size for t in self.sites)
+
+    def copy(self) -> "MpsState":
+        return MpsState(
+            [t.copy() for t in self.sites], self.trunc_budget_per_gate, self.accumulated_discard,
+            self.ortho_center, self.peak_chi, self.gate_count_1q, self.gate_count_2q, dict(self.timings),
+        )
+
+
+@dataclass(frozen=True)
+class SimStats:
+    max_chi: int
+    entry_count: int
+    memory_bytes: int
+    gate_count_1q: int
+    gate_count_2q: int
+    wall_time_per_phase: dict
+
+
+def init_state(m: int, basis: str = "zero", trunc_budget_per_gate: float = DEFAULT_TRUNC_BUDGET) -> MpsState:
+    """|0...0> or |+>^m product state (mps.py:90-102)."""
+    if m < 1:
+        raise ValueError("qubit count must be at least 1")
+    vecs = {"zero": [1.0, 0.0], "plus": [2**-0.5, 2**-0.5]}
+    if basis not in vecs:
+        raise ValueError(f"unknown basis {basis!r}; use 'zero' or 'plus'")
+    v = np.array(vecs[basis], dtype=np.complex128).reshape(1, 2, 1)
+    return MpsState([v.copy() for _ in range(m)], trunc_budget_per_gate=trunc_budget_per_gate, ortho_center=0)
+
+
+def stats(state: MpsState) -> SimStats:
+    """Resource counters (mps.py:281-291); memory is 16 bytes per entry."""
+    n = state.entry_count()
+    return SimStats(
+        max(state.peak_chi, state.max_bond()), n, 16 * n, state.gate_count_1q, state.gate_count_2q,
+        dict(state.timings),
+    )
+
+
+def to_statevector(state: MpsState) -> np.ndarray:
+    """Dense amplitudes, qubit 0 most significant (host test aid, mps.py:271-278)."""
+    if state.m > _MAX_DENSE_QUBITS:
+        raise ValueError(f"refusing dense conversion beyond {_MAX_DENSE_QUBITS} qubits")
+    psi = np.ones((1, 1), dtype=np.complex128)
+    for t in state.sites:
+        psi = np.einsum("xa,apb->xpb", psi, t).reshape(-1, t.shape[2])
+    return psi.reshape(-1)
+
+
+# ---------------------------------------------------------------- programs
+@dataclass(frozen=True)
+class Program:
+    """A gate topology compiled into the op list replayed by the GPU."""
+
+    m: int
+    ops: np.ndarray  # (n_ops, 4) int32
+    n_gates: int
+    n_params: int
+    n_qr_left: int
+    n_qr_right: int
+    final_center: int
+    gate_count_1q: int
+    gate_count_2q: int
+
+    @functools.cached_property
+    def device_ops(self) -> torch.Tensor:
+        return torch.from_numpy(self.ops).to("cuda")
+
+
+def _topology_key(topo: Topology):
+    return (topo.m, topo.kinds.tobytes(), topo.q0.tobytes(), topo.q1.tobytes(), topo.param_slot.tobytes())
+
+
+_PROGRAMS: dict = {}
+_CAP_HINT: dict = {}
+
+
+def compile_program(topo: Topology) -> Program:
+    key = _topology_key(topo)
+    prog = _PROGRAMS.get(key)
+    if prog is not None:
+        return prog
+    lib = N.lib()
+    kinds = np.ascontiguousarray(topo.kinds, dtype=np.int32)
+    q0 = np.ascontiguousarray(topo.q0, dtype=np.int32)
+    q1 = np.ascontiguousarray(topo.q1, dtype=np.int32)
+    slot = np.ascontiguousarray(topo.param_slot, dtype=np.int32)
+    args = [N.ptr(a, N.C.c_int32) for a in (kinds, q0, q1, slot)]
+    n_ops, nl, nr = N.C.c_int64(0), N.C.c_int64(0), N.C.c_int64(0)
+    N.check(lib.mpskq_program_compile(topo.m, kinds.size, *args, None, 0, N.C.byref(n_ops), None, None))
+    ops = np.zeros((n_ops.value, 4), dtype=np.int32)
+    N.check(
+        lib.mpskq_program_compile(
+            topo.m, kinds.size, *args, N.ptr(ops, N.C.c_int32), n_ops.value, N.C.byref(n_ops),
+            N.C.byref(nl), N.C.byref(nr),
+        )
+    )
+    center = 0
+    for code, site, _, _ in ops:
+        c = code & 0xFF
+        if c in (3, 4):  # two-qubit ops: center ends on the absorbing side
+            center = site if (code >> 8) & 1 else site + 1
+    two = np.isin(kinds, (N.GATE_RXX, N.GATE_SWAP))
+    prog = Program(topo.m, ops, int(kinds.size), int(topo.n_params), int(nl.value), int(nr.value), center,
+                   int((~two).sum()), int(two.sum()))
+    _PROGRAMS[key] = prog
+    return prog
+
+
+def batch_layout(m: int, chi_cap: int) -> tuple:
+    off = np.zeros(m + 1, dtype=np.int64)
+    stride = N.C.c_int64(0)
+    N.check(N.lib().mpskq_batch_layout(m, chi_cap, N.ptr(off, N.C.c_int64), N.C.byref(stride)))
+    return off, int(stride.value)
+
+
+# ---------------------------------------------------------------- device batch
+class MpsBatch(Sequence):
+    """Device-resident batch of MPS produced by the GPU simulator.
+
+    Storage (see include/mpskq.h): one complex128 slab with per-site slots,
+    ``chi`` bond dims (n, m+1).  Indexing returns host ``MpsState`` copies in
+    the reference layout.
+    """
+
+    def __init__(self, m, chi_cap, site_off, stride, sites, chi, discard, peak, budget,
+                 gate_count_1q, gate_count_2q, ortho_center, entry_log=None, seconds=0.0):
+        self.m = m
+        self.chi_cap = chi_cap
+        self.site_off = site_off
+        self.site_off_dev = torch.from_numpy(site_off).to(sites.device)
+        self.stride = stride
+        self.sites = sites  # float64 (n, 2*stride)
+        self.chi = chi  # int32 (n, m+1)
+        self.discard = discard  # float64 (n,)
+        self.peak = peak  # int32 (n,)
+        self.budget = budget
+        self.gate_count_1q = gate_count_1q
+        self.gate_count_2q = gate_count_2q
+        self.ortho_center = ortho_center
+        self.entry_log = entry_log
+        self.seconds = seconds
+        self._host = None
+
+    def __len__(self) -> int:
+        return self.chi.shape[0]
+
+    def _host_arrays(self):
+        if self._host is None:
+            self._host = (
+                self.sites.cpu().numpy().view(np.complex128),
+                self.chi.cpu().numpy(),
+                self.discard.cpu().numpy(),
+                self.peak.cpu().numpy(),
+            )
+        return self._host
+
+    def bond_dims(self) -> np.ndarray:
+        return self._host_arrays()[1]
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[k] for k in range(*i.indices(len(self)))]
+        n = len(self)
+        if i < 0:
+            i += n
+        if not 0 <= i < n:
+            raise IndexError(i)
+        sites, chi, disc, peak = self._host_arrays()
+        row, c = sites[i], chi[i]
+        ts = [
+            row[self.site_off[s] : self.site_off[s] + c[s] * 2 * c[s + 1]].reshape(c[s], 2, c[s + 1]).copy()
+            for s in range(self.m)
+        ]
+        per = self.seconds / max(n, 1)
+        return MpsState(ts, self.budget, float(disc[i]), self.ortho_center, int(peak[i]), self.gate_count_1q,
+                        self.gate_count_2q, {"simulation": per})
+
+    def rows(self, a: int, b: int) -> "MpsBatch":
+        """Device view of states a..b-1 (no copy)."""
+        log = None if self.entry_log is None else self.entry_log[a:b]
+        return MpsBatch(self.m, self.chi_cap, self.site_off, self.stride, self.sites[a:b], self.chi[a:b],
+                        self.discard[a:b], self.peak[a:b], self.budget, self.gate_count_1q,
+                        self.gate_count_2q, self.ortho_center, log, self.seconds * (b - a) / max(len(self), 1))
+
+    def to_states(self) -> list:
+        return [self[i] for i in range(len(self))]
+
+    def memory_log(self, i: int) -> list:
+        if self.entry_log is None:
+            raise ValueError("batch was simulated without a memory log")
+        return [16 * int(x) for x in self.entry_log[i].cpu().numpy()]
+
+    @classmethod
+    def from_states(cls, states, chi_cap: int | None = None) -> "MpsBatch":
+        """Upload host MpsState objects (e.g. produced by the reference) into a batch."""
+        require_cuda()
+        states = list(states)
+        if not states:
+            raise ValueError("no states")
+        m = states[0].m
+        if any(s.m != m for s in states):
+            raise ValueError("qubit count mismatch between state lists")
+        need = max(max(s.bond_dims()) for s in states)
+        caps = N.supported_chi_caps()
+        if chi_cap is None:
+            chi_cap = next((c for c in caps if c >= need), None)
+            if chi_cap is None:
+                raise ValueError(f"bond dimension {need} exceeds the largest compiled capacity {caps[-1]}")
+        elif chi_cap < need:
+            raise ValueError(f"bond dimension {need} exceeds chi capacity {chi_cap}")
+        off, stride = batch_layout(m, chi_cap)
+        host = np.zeros((len(states), stride), dtype=np.complex128)
+        chi = np.zeros((len(states), m + 1), dtype=np.int32)
+        for n, s in enumerate(states):
+            chi[n] = s.bond_dims()
+            for k, t in enumerate(s.sites):
+                host[n, off[k] : off[k] + t.size] = np.asarray(t, dtype=np.complex128).reshape(-1)
+        dev = torch.device("cuda")
+        return cls(
+            m, chi_cap, off, stride, torch.from_numpy(host.view(np.float64)).to(dev), torch.from_numpy(chi).to(dev),
+            torch.tensor([s.accumulated_discard for s in states], dtype=torch.float64, device=dev),
+            torch.tensor([s.peak_chi for s in states], dtype=torch.int32, device=dev),
+            states[0].trunc_budget_per_gate, states[0].gate_count_1q, states[0].gate_count_2q,
+            states[0].ortho_center,
+        )
+
+
+def simulate_program(prog: Program, coef, budget: float, chi_max: int = 0,
+                     chi_cap: int | None = None, memory_log: bool = False) -> MpsBatch:
+    """Run the compiled program from |0..0> for every row of the coefficient
+    table ``coef`` ((n, n_params, 2) half-angle cos/sin, numpy or a CUDA
+    tensor); escalates the chi capacity on overflow."""
+    require_cuda()
+    if budget < 0:
+        raise ValueError("budget must be non-negative")
+    dev = torch.device("cuda")
+    if not isinstance(coef, torch.Tensor):
+        coef = torch.from_numpy(np.ascontiguousarray(coef, dtype=np.float64))
+    coef = coef.to(dev, torch.float64).contiguous()
+    if coef.ndim != 3 or tuple(coef.shape[1:]) != (prog.n_params, 2):
+        raise ValueError(f"coefficient table must be (n, {prog.n_params}, 2), got {tuple(coef.shape)}")
+    n = coef.shape[0]
+    coef_d = coef if coef.numel() else torch.zeros(2, dtype=torch.float64, device=dev)
+    ops_d = prog.device_ops
+    caps = N.supported_chi_caps()
+    key = id(prog)
+    if chi_cap is not None:
+        if chi_cap not in caps:
+            raise ValueError(f"chi capacity {chi_cap} is not compiled in (have {caps})")
+        order = [chi_cap]
+    else:
+        order = [c for c in caps if c >= _CAP_HINT.get(key, caps[0])]
+        if chi_max > 0:  # the kept rank never exceeds chi_max
+            order = [c for c in order if c < chi_max] + [c for c in order if c >= chi_max][:1]
+    m = prog.m
+    for cap in order:
+        off, stride = batch_layout(m, cap)
+        off_d = torch.from_numpy(off).to(dev)
+        sites = torch.empty((n, 2 * stride), dtype=torch.float64, device=dev)
+        chi = torch.empty((n, m + 1), dtype=torch.int32, device=dev)
+        disc = torch.empty(n, dtype=torch.float64, device=dev)
+        peak = torch.empty(n, dtype=torch.int32, device=dev)
+        status = torch.zeros(n, dtype=torch.int32, device=dev)
+        elog = torch.zeros((n, prog.n_gates), dtype=torch.int64, device=dev) if memory_log else None
+        with Timer() as tm:
+            N.check(
+                N.lib().mpskq_simulate(
+                    m, cap, dptr(ops_d), prog.ops.shape[0], prog.n_gates, dptr(coef_d), prog.n_params, n,
+                    float(budget), int(chi_max), dptr(off_d), stride, dptr(sites), dptr(chi), dptr(disc),
+                    dptr(peak), dptr(status), dptr(elog), stream_ptr(),
+                )
+            )
+        st = status.cpu().numpy()
+        if np.any(st == N.STATE_NONFINITE):
+            raise ValueError("tensor has non-finite entries")
+        if np.any(st == N.STATE_CAPACITY):
+            continue
+        _CAP_HINT[key] = cap
+        return MpsBatch(m, cap, off, stride, sites, chi, disc, peak, budget, prog.gate_count_1q,
+                        prog.gate_count_2q, prog.final_center, elog, tm.seconds())
+    raise RuntimeError(f"bond dimension exceeds the largest usable chi capacity {order[-1]}")
+
+
+def simulate_circuit(circuit: Circuit, budget: float = DEFAULT_TRUNC_BUDGET, memory_log: list | None = None) -> MpsState:
+    """Simulate ``circuit`` from |0...0> on the GPU (mps.py:250-257)."""
+    topo, angles = circuit_topology(circuit)
+    prog = compile_program(topo)
+    coef = half_angle_coefficients(angles).reshape(1, -1, 2)
+    batch = simulate_program(prog, coef, budget, memory_log=memory_log is not None)
+    if memory_log is not None:
+        memory_log.extend(batch.memory_log(0))
+    return batch[0]
+
+
+def _as_batch(x) -> tuple:
+    if isinstance(x, MpsBatch):
+        return x, None
+    if isinstance(x, MpsState):
+        return MpsBatch.from_states([x]), None
+    raise TypeError(f"expected MpsState or MpsBatch, got {type(x).__name__}")
+
+
+def overlap_matrix(bras: MpsBatch, kets: MpsBatch, kind: str, amplitude: bool = False,
+                   rank: int = 0, world: int = 1, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Device matrix of |<bra_i|ket_j>|^2 (or the complex amplitudes)."""
+    require_cuda()
+    if bras.m != kets.m:
+        raise ValueError("qubit count mismatch between state lists")
+    if bras.chi_cap != kets.chi_cap:
+        cap = max(bras.chi_cap, kets.chi_cap)
+        bras = bras if bras.chi_cap == cap else MpsBatch.from_states(bras.to_states(), cap)
+        kets = kets if kets.chi_cap == cap else MpsBatch.from_states(kets.to_states(), cap)
+    kind_id = N.KIND_TRAIN if kind == "train" else N.KIND_TEST
+    nb, nk = len(bras), len(kets)
+    if out is None:
+        shape = (nb, nk, 2) if amplitude else (nb, nk)
+        out = torch.zeros(shape, dtype=torch.float64, device=bras.sites.device)
+    N.check(
+        N.lib().mpskq_overlap(
+            kind_id, N.OUT_AMPLITUDE if amplitude else N.OUT_KERNEL, bras.m, bras.chi_cap,
+            dptr(bras.site_off_dev), bras.stride, dptr(bras.sites), dptr(bras.chi), nb,
+            dptr(kets.sites), dptr(kets.chi), nk, rank, world, dptr(out), nk, stream_ptr(),
+        )
+    )
+    return out
+
+
+def inner_product(bra, ket) -> complex:
+    """<bra|ket> with the bra conjugated, contracted site by site (mps.py:260-268)."""
+    if bra.m != ket.m:
+        raise ValueError(f"qubit count mismatch: {bra.m} vs {ket.m}")
+    b, _ = _as_batch(bra)
+    k, _ = _as_batch(ket)
+    if len(b) != 1 or len(k) != 1:
+        raise ValueError("inner_product takes single states")
+    amp = overlap_matrix(b, k, "test", amplitude=True).cpu().numpy()
+    return complex(amp[0, 0, 0], amp[0, 0, 1])

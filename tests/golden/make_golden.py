@@ -1,0 +1,208 @@
+"""Generate the golden fixtures of the parity suite from the REAL reference.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports the unmodified reference package from /root/reference/pkg/src and
+records its outputs for seeded inputs into tests/golden/*.npz.  The GPU box
+never reads /root/reference: the tests only load these committed files.
+"""
+
+from __future__ import annotations
+
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+OUT = Path(__file__).resolve().parent
+sys.path.insert(0, str(REF))
+
+from mpskernel import ansatz, kernel, mps, tensor  # noqa: E402
+
+
+def pack_states(states):
+    """Flatten a list of MpsState into arrays (bond dims, offsets, entries)."""
+    m = states[0].m
+    chi = np.array([s.bond_dims() for s in states], dtype=np.int32)
+    data, offs = [], []
+    off = 0
+    for s in states:
+        row = []
+        for t in s.sites:
+            row.append(off)
+            data.append(t.reshape(-1))
+            off += t.size
+        offs.append(row)
+    return dict(
+        chi=chi,
+        site_off=np.array(offs, dtype=np.int64).reshape(len(states), m),
+        entries=np.concatenate(data).astype(np.complex128),
+        discard=np.array([s.accumulated_discard for s in states]),
+        peak=np.array([s.peak_chi for s in states], dtype=np.int32),
+        g1=np.array([s.gate_count_1q for s in states], dtype=np.int64),
+        g2=np.array([s.gate_count_2q for s in states], dtype=np.int64),
+    )
+
+
+def gram_case(name, m, r, d, gamma, budget, n_train, n_test, seed, keep_states=False):
+    t0 = time.time()
+    cfg = ansatz.FeatureMapConfig(m, r, d, gamma)
+    rng = np.random.default_rng(seed)
+    X = rng.uniform(0.0, 2.0, (n_train, m))
+    Xt = rng.uniform(0.0, 2.0, (n_test, m))
+    train = kernel.simulate_dataset(X, cfg, budget=budget)
+    test = kernel.simulate_dataset(Xt, cfg, budget=budget)
+    Ktr = kernel.compute_gram(train, train, "train").entries
+    Kte = kernel.compute_gram(test, train, "test").entries
+    amp = np.array([[mps.inner_product(a, b) for b in train[:4]] for a in test[:4]])
+    circ = ansatz.encode_circuit(X[0], cfg)
+    out = dict(
+        m=m, r=r, d=d, gamma=gamma, budget=budget, X=X, X_test=Xt, K_train=Ktr, K_test=Kte,
+        amp_test4=amp,
+        kinds=np.array([ansatz.GATE_KINDS.index(g.kind) for g in circ.gates], dtype=np.int32),
+        q0=np.array([g.qubits[0] for g in circ.gates], dtype=np.int32),
+        q1=np.array([g.qubits[1] if len(g.qubits) > 1 else -1 for g in circ.gates], dtype=np.int32),
+        angles0=np.array([np.nan if g.angle is None else g.angle for g in circ.gates]),
+    )
+    for key, val in pack_states(train).items():
+        if key in ("entries", "site_off") and not keep_states:
+            continue
+        out["train_" + key] = val
+    for key, val in pack_states(test).items():
+        if key in ("entries", "site_off"):
+            continue
+        out["test_" + key] = val
+    np.savez_compressed(OUT / f"{name}.npz", **out)
+    print(f"{name}: {time.time() - t0:.1f}s  max chi {out['train_chi'].max()}")
+
+
+def svd_cases():
+    """svd_truncated on matrices with prescribed spectra (tensor.py:87-123)."""
+    rng = np.random.default_rng(7)
+    mats, budgets, keeps, svals, discs, shapes = [], [], [], [], [], []
+
+    def rand_unitary(n):
+        q, _ = np.linalg.qr(rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n)))
+        return q
+
+    specs = [
+        (4, 4, [1.0, 0.5, 0.25, 0.125], 0.0),
+        (4, 4, [1.0, 0.5, 1e-9, 0.0], 0.0),
+        (4, 4, [1.0, 0.5, 1e-9, 1e-18], 1e-30),
+        (4, 4, [1.0, 1e-13, 1e-13, 1e-13], 1e-24),
+        (8, 8, [1.0, 0.3, 0.1, 1e-5, 1e-8, 1e-11, 1e-13, 1e-16], 1e-24),
+        (8, 6, [1.0, 0.3, 0.1, 1e-5, 1e-8, 1e-11], 1e-16),
+        (6, 8, [1.0, 0.3, 0.1, 1e-5, 1e-8, 1e-11], 1e-20),
+        (8, 8, [1.0] * 8, 0.5),
+        (8, 8, [1.0] + [1e-16] * 7, 0.0),
+        (16, 16, list(np.geomspace(1.0, 1e-15, 16)), 1e-24),
+        (32, 32, list(np.geomspace(1.0, 1e-14, 32)), 1e-16),
+        (16, 12, list(np.geomspace(1.0, 1e-10, 12)), 1e-18),
+    ]
+    for rows, cols, sv, budget in specs:
+        k = min(rows, cols)
+        u = rand_unitary(rows)[:, :k]
+        v = rand_unitary(cols)[:k, :]
+        mat = (u * np.array(sv)) @ v
+        res = tensor.svd_truncated(mat.reshape(rows, cols), 1, budget)
+        mats.append(mat.reshape(-1))
+        budgets.append(budget)
+        keeps.append(res.singular_values.size)
+        s = np.zeros(k)
+        s[: res.singular_values.size] = res.singular_values
+        svals.append(s)
+        discs.append(res.discarded_weight)
+        shapes.append((rows, cols))
+    np.savez_compressed(
+        OUT / "svd_cases.npz",
+        mats=np.array(mats, dtype=object),
+        shapes=np.array(shapes, dtype=np.int32),
+        budgets=np.array(budgets),
+        keeps=np.array(keeps, dtype=np.int32),
+        svals=np.array(svals, dtype=object),
+        discarded=np.array(discs),
+        allow_pickle=True,
+    )
+    print("svd_cases:", len(specs))
+
+
+def schedule_cases():
+    """make_schedule outputs for API parity (kernel.py:316-333)."""
+    rows = []
+    for strategy in ("round_robin", "no_messaging"):
+        for kind, nb, nk in [("train", 5, 5), ("train", 16, 16), ("test", 4, 16), ("test", 3, 10)]:
+            for k in (1, 2, 3, 4, 6):
+                s = kernel.make_schedule(nb, nk, k, strategy, kind)
+                tiles = [
+                    (si, t.worker, t.row_start, t.row_stop, t.col_start, t.col_stop)
+                    for si, st in enumerate(s.steps)
+                    for t in st.tiles
+                ]
+                transfers = [
+                    (si, t.src, t.dst, t.which, t.start, t.stop)
+                    for si, st in enumerate(s.steps)
+                    for t in st.transfers
+                ]
+                rows.append(
+                    dict(strategy=strategy, kind=kind, nb=nb, nk=nk, k=k, kk=s.k,
+                         initial={str(w): v for w, v in s.initial_states.items()},
+                         tiles=tiles, transfers=transfers)
+                )
+    import json
+
+    (OUT / "schedules.json").write_text(json.dumps(rows))
+    print("schedules:", len(rows))
+
+
+def kernel_fixture():
+    """The reference's own test fixture: test_kernel.py:23-34 (m=6, r=1, d=2, gamma=0.5)."""
+    cfg = ansatz.FeatureMapConfig(6, 1, 2, 0.5)
+    X = np.random.default_rng(42).uniform(0.0, 2.0, (8, 6))
+    states = kernel.simulate_dataset(X, cfg)
+    K = kernel.compute_gram(states, states, "train").entries
+    sv = [mps.to_statevector(s) for s in states]
+    np.savez_compressed(OUT / "kernel_fixture.npz", X=X, K=K, chi=np.array([s.bond_dims() for s in states]),
+                        statevectors=np.array(sv))
+    print("kernel_fixture")
+
+
+def acceptance_c1():
+    """Acceptance criterion 1's random small configs (test_acceptance.py:41-75), seed 20240901."""
+    rng = np.random.default_rng(20240901)
+    cases = []
+    for _ in range(50):
+        m = int(rng.integers(2, 11))
+        d = int(rng.integers(1, min(4, m - 1) + 1))
+        r = int(rng.integers(1, 4))
+        gamma = float(rng.choice([0.1, 0.5, 1.0]))
+        X = rng.uniform(0.0, 2.0, (3, m))
+        cfg = ansatz.FeatureMapConfig(m, r, d, gamma)
+        states = kernel.simulate_dataset(X, cfg)
+        K = kernel.compute_gram(states, states, "train").entries
+        cases.append(dict(m=m, r=r, d=d, gamma=gamma, X=X.tolist(), K=K.tolist(),
+                          chi=[s.bond_dims() for s in states],
+                          discard=[s.accumulated_discard for s in states]))
+    import json
+
+    (OUT / "acceptance_c1.json").write_text(json.dumps(cases))
+    print("acceptance_c1:", len(cases))
+
+
+if __name__ == "__main__":
+    OUT.mkdir(parents=True, exist_ok=True)
+    svd_cases()
+    schedule_cases()
+    kernel_fixture()
+    acceptance_c1()
+    # config 1: m=8, d=1 (BASELINE "r=1" = interaction distance), 2 layers, untruncated
+    gram_case("config1_m8_d1", 8, 2, 1, 0.5, 0.0, 64, 16, seed=0, keep_states=True)
+    # headline shape (config 4), subset of rows: m=165, d=1, 2 layers, gamma 0.1, budget 1e-24
+    gram_case("headline_m165_d1", 165, 2, 1, 0.1, 1e-24, 24, 8, seed=0, keep_states=True)
+    # config 2 shape: m=50, d=2, budget 1e-24
+    gram_case("config2_m50_d2", 50, 2, 2, 0.1, 1e-24, 24, 8, seed=0)
+    # config 3 shape: m=100, d=4, fidelity cutoff 1e-16
+    gram_case("config3_m100_d4", 100, 2, 4, 0.1, 1e-16, 10, 4, seed=0)
