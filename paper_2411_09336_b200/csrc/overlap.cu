@@ -89,47 +89,98 @@ __device__ __forceinline__ void store_result(int out_mode, double* out, int64_t 
 }
 
 // --------------------------------------------------------------- small chi
+// bra-major padded layout [site][state (padded to the 8-bra tile)][entry]: the
+// 8 bras of a tile at one site are one contiguous 4 KB run for a bulk copy
+__global__ void pack_bra_kernel(const double2* __restrict__ sites, const int32_t* __restrict__ chi,
+                                const int64_t* __restrict__ site_off, int64_t stride, int m,
+                                int64_t n, int64_t n_pad, double2* __restrict__ out) {
+  const int64_t total = (int64_t)m * n_pad * kEnt;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int e = (int)(idx % kEnt);
+    const int64_t state = (idx / kEnt) % n_pad;
+    const int s = (int)(idx / ((int64_t)kEnt * n_pad));
+    double2 v = make_double2(0.0, 0.0);
+    if (state < n) {
+      const int k = e / (2 * kP), p = (e / kP) & 1, r = e % kP;
+      const int chl = chi[state * (m + 1) + s], chr = chi[state * (m + 1) + s + 1];
+      if (k < chl && r < chr) v = sites[state * stride + site_off[s] + (k * 2 + p) * chr + r];
+    }
+    out[idx] = v;
+  }
+}
+
+constexpr int kStages = 4;
+constexpr uint32_t kKetBytes = kEnt * kLanes * sizeof(double2);   // 16 KB per site
+constexpr uint32_t kBraBytes = kWarpsO1 * kEnt * sizeof(double2);  // 4 KB per site
+constexpr size_t kO1Smem = kStages * (size_t)(kKetBytes + kBraBytes) + kStages * sizeof(uint64_t);
+
 struct O1Args {
-  const double2* bra;  // packed
-  const double2* ket;  // packed
+  const double2* bra;  // [site][n_pad_bra][entry]
+  const double2* ket;  // [site][nblk_ket][entry][lane]
   const int32_t* bra_chi;
   const int32_t* ket_bmax;
-  int64_t n_bras, n_kets, nblk_bra, nblk_ket;
+  int64_t n_bras, n_kets, n_pad_bra, nblk_ket;
   int m, kind, out_mode;
-  const int2* tiles;  // (bra tile, ket block)
+  const int2* tiles;  // (bra tile of 8, ket block of 32)
   int64_t n_tiles;
   double* out;
   int64_t ld;
 };
 
+// One CTA = 8 bras (warps) x 32 kets (lanes); one thread owns one pair's 4x4
+// complex environment in registers.  Thread 0 streams each site's ket block
+// (16 KB) and bra tile (4 KB) into a 4-stage shared-memory ring with TMA bulk
+// copies signalled on mbarriers, kStages-1 sites ahead of the compute.
 __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) {
-  __shared__ double2 sA[kWarpsO1][kEnt];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* sket = reinterpret_cast<double2*>(smem_raw);
+  double2* sbra = sket + kStages * kEnt * kLanes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sbra + kStages * kWarpsO1 * kEnt);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m = a.m;
+  if (tid == 0) {
+    for (int q = 0; q < kStages; ++q) mbar_init(&full[q], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int64_t kstride = a.nblk_ket * kEnt * kLanes;  // per site
+  const int64_t bstride = a.n_pad_bra * kEnt;
+  uint32_t it = 0;  // sites consumed by this CTA so far (ring position + phase)
   for (int64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
     const int2 tile = a.tiles[t];
+    const double2* kbase = a.ket + (int64_t)tile.y * kEnt * kLanes;
+    const double2* bbase = a.bra + (int64_t)tile.x * kWarpsO1 * kEnt;
+    auto issue = [&](int site, uint32_t q) {
+      const uint32_t buf = q % kStages;
+      mbar_arrive_expect_tx(&full[buf], kKetBytes + kBraBytes);
+      bulk_g2s(sket + buf * kEnt * kLanes, kbase + site * kstride, kKetBytes, &full[buf]);
+      bulk_g2s(sbra + buf * kWarpsO1 * kEnt, bbase + site * bstride, kBraBytes, &full[buf]);
+    };
+    if (tid == 0)
+      for (int s = 0; s < kStages - 1 && s < m; ++s) issue(s, it + s);
+
     const int64_t i = (int64_t)tile.x * kWarpsO1 + warp;  // bra (warp-uniform)
     const int64_t j = (int64_t)tile.y * kLanes + lane;    // ket (per lane)
     const int64_t ic = i < a.n_bras ? i : a.n_bras - 1;
     const int32_t* bchi = a.bra_chi + ic * (m + 1);
     const int32_t* kmax = a.ket_bmax + (int64_t)tile.y * (m + 1);
-    const int64_t ib = ic / kLanes, il = ic % kLanes;
 
     double2 env[kP][kP];
 #pragma unroll
     for (int x = 0; x < kP; ++x)
 #pragma unroll
       for (int y = 0; y < kP; ++y) env[x][y] = make_double2(x == 0 && y == 0 ? 1.0 : 0.0, 0.0);
-
-    int na = 1, nb = 1;  // chi_s of bra / ket block
+    int na = 1, nb = 1;  // chi_s of the bra / of the ket block
     for (int s = 0; s < m; ++s) {
+      if (tid == 0 && s + kStages - 1 < m) issue(s + kStages - 1, it + kStages - 1);
       const int na1 = __ldg(bchi + s + 1);
       const int nb1 = __ldg(kmax + s + 1);
-      // stage this warp's bra tensor (conjugated on use) in shared memory
-      sA[warp][lane] =
-          __ldg(a.bra + (((int64_t)s * a.nblk_bra + ib) * kEnt + lane) * kLanes + il);
-      __syncwarp();
-      const double2* kp = a.ket + (((int64_t)s * a.nblk_ket + tile.y) * kEnt) * kLanes + lane;
+      const uint32_t buf = it % kStages;
+      mbar_wait(&full[buf], (it / kStages) & 1);
+      ++it;
+      const double2* B = sket + buf * kEnt * kLanes + lane;  // B[e] at B[e * 32]
+      const double2* A = sbra + buf * kWarpsO1 * kEnt + warp * kEnt;
       double2 nenv[kP][kP];
 #pragma unroll
       for (int x = 0; x < kP; ++x)
@@ -138,18 +189,16 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
 #pragma unroll
       for (int br = 0; br < kP; ++br) {
         if (br < nb1) {
-          // column br of the ket tensor: B[kb][p][br]
-          double2 Bc[kP][2];
+          double2 Bc[kP][2];  // column br of the ket tensor: B[kb][p][br]
 #pragma unroll
           for (int kb = 0; kb < kP; ++kb)
 #pragma unroll
             for (int p = 0; p < 2; ++p)
-              Bc[kb][p] = kb < nb ? __ldg(kp + ((kb * 2 + p) * kP + br) * kLanes)
-                                  : make_double2(0.0, 0.0);
+              Bc[kb][p] = kb < nb ? B[((kb * 2 + p) * kP + br) * kLanes] : make_double2(0.0, 0.0);
           // T[al][p] = sum_kb env[al][kb] B[kb][p][br]
           double2 T[kP][2];
 #pragma unroll
-          for (int al = 0; al < kP; ++al) {
+          for (int al = 0; al < kP; ++al)
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
               double2 acc = make_double2(0.0, 0.0);
@@ -160,21 +209,18 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
               }
               T[al][p] = acc;
             }
-          }
-          // nenv[ar][br] = sum_{al,p} conj(A[al][p][ar]) T[al][p]
+          // nenv[ar][br] = sum_{al,p} conj(A[al][p][ar]) T[al][p]  (two partial chains)
 #pragma unroll
           for (int ar = 0; ar < kP; ++ar) {
             if (ar < na1) {
-              double2 acc = make_double2(0.0, 0.0);
+              double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
 #pragma unroll
-              for (int al = 0; al < kP; ++al) {
+              for (int al = 0; al < kP; ++al)
                 if (al < na) {
-#pragma unroll
-                  for (int p = 0; p < 2; ++p)
-                    acc = cfmac(sA[warp][(al * 2 + p) * kP + ar], T[al][p], acc);
+                  acc0 = cfmac(A[(al * 2 + 0) * kP + ar], T[al][0], acc0);
+                  acc1 = cfmac(A[(al * 2 + 1) * kP + ar], T[al][1], acc1);
                 }
-              }
-              nenv[ar][br] = acc;
+              nenv[ar][br] = cadd(acc0, acc1);
             }
           }
         }
@@ -185,7 +231,7 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
         for (int y = 0; y < kP; ++y) env[x][y] = nenv[x][y];
       na = na1;
       nb = nb1;
-      __syncwarp();
+      __syncthreads();  // every warp is done with `buf` before it is refilled
     }
     const bool train = a.kind == MPSKQ_KIND_TRAIN;
     const bool valid = i < a.n_bras && j < a.n_kets && (!train || i < j);
@@ -315,52 +361,56 @@ int grid_for(int64_t n_tiles, int per_sm) {
 
 int launch_o1(const OverlapArgs& a, cudaStream_t st) {
   const int m = a.m;
-  const bool same = a.bra_sites == a.ket_sites;
-  const int64_t nbb = (a.n_bras + kLanes - 1) / kLanes, nbk = (a.n_kets + kLanes - 1) / kLanes;
-  const size_t pb = sizeof(double2) * (size_t)m * nbb * kEnt * kLanes;
-  const size_t pk = sizeof(double2) * (size_t)m * nbk * kEnt * kLanes;
+  const int64_t npb = (a.n_bras + kWarpsO1 - 1) / kWarpsO1 * kWarpsO1;
+  const int64_t nbk = (a.n_kets + kLanes - 1) / kLanes;
+  const size_t bb = sizeof(double2) * (size_t)m * npb * kEnt;
+  const size_t kb = sizeof(double2) * (size_t)m * nbk * kEnt * kLanes;
   void *bra = nullptr, *ket = nullptr, *kmax = nullptr;
-  cudaError_t e = cudaMallocAsync(&bra, pb, st);
+  cudaError_t e = cudaMallocAsync(&bra, bb, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(packed bras)");
-  if (!same) {
-    e = cudaMallocAsync(&ket, pk, st);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(packed kets)");
-  } else {
-    ket = bra;
-  }
+  e = cudaMallocAsync(&ket, kb, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(packed kets)");
   e = cudaMallocAsync(&kmax, sizeof(int32_t) * nbk * (m + 1), st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(block chi)");
   const int threads = 256;
-  auto pack = [&](const double* sites, const int32_t* chi, int64_t n, int64_t nblk, void* out) {
-    const int64_t total = (int64_t)m * nblk * kEnt * kLanes;
-    const int blocks = (int)std::min<int64_t>((total + threads - 1) / threads, 148 * 64);
-    pack_o1_kernel<<<blocks, threads, 0, st>>>(reinterpret_cast<const double2*>(sites), chi,
-                                               a.site_off, a.state_stride, m, n, nblk,
-                                               static_cast<double2*>(out));
+  auto blocks_for = [&](int64_t total) {
+    return (int)std::min<int64_t>((total + threads - 1) / threads, 148 * 64);
   };
-  pack(a.bra_sites, a.bra_chi, a.n_bras, nbb, bra);
-  if (!same) pack(a.ket_sites, a.ket_chi, a.n_kets, nbk, ket);
-  {
-    const int64_t total = nbk * (m + 1);
-    const int blocks = (int)std::min<int64_t>((total + threads - 1) / threads, 148 * 16);
-    block_max_chi_kernel<<<blocks, threads, 0, st>>>(a.ket_chi, m, a.n_kets, nbk,
-                                                     static_cast<int32_t*>(kmax));
-  }
+  pack_bra_kernel<<<blocks_for((int64_t)m * npb * kEnt), threads, 0, st>>>(
+      reinterpret_cast<const double2*>(a.bra_sites), a.bra_chi, a.site_off, a.state_stride, m,
+      a.n_bras, npb, static_cast<double2*>(bra));
+  pack_o1_kernel<<<blocks_for((int64_t)m * nbk * kEnt * kLanes), threads, 0, st>>>(
+      reinterpret_cast<const double2*>(a.ket_sites), a.ket_chi, a.site_off, a.state_stride, m,
+      a.n_kets, nbk, static_cast<double2*>(ket));
+  block_max_chi_kernel<<<blocks_for(nbk * (m + 1)), threads, 0, st>>>(a.ket_chi, m, a.n_kets, nbk,
+                                                                      static_cast<int32_t*>(kmax));
   const bool train = a.kind == MPSKQ_KIND_TRAIN;
   auto tiles = make_tiles(train, a.n_bras, a.n_kets, kWarpsO1, kLanes, a.rank, a.world);
   int2* dtiles = nullptr;
   if (int s = upload_tiles(tiles, &dtiles, st)) return s;
   if (!tiles.empty()) {
+    static bool attr = false;
+    if (!attr) {
+      e = cudaFuncSetAttribute(overlap_o1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kO1Smem);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(o1)");
+      attr = true;
+    }
     O1Args o{static_cast<const double2*>(bra), static_cast<const double2*>(ket), a.bra_chi,
-             static_cast<const int32_t*>(kmax), a.n_bras, a.n_kets, nbb, nbk, m, a.kind,
+             static_cast<const int32_t*>(kmax), a.n_bras, a.n_kets, npb, nbk, m, a.kind,
              a.out_mode, dtiles, (int64_t)tiles.size(), a.out, a.ld};
-    overlap_o1_kernel<<<grid_for((int64_t)tiles.size(), 1), kWarpsO1 * 32, 0, st>>>(o);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // persistent: one CTA per SM walks the tile list (the ring stays warm)
+    const int grid = (int)std::min<int64_t>((int64_t)tiles.size(), sms);
+    overlap_o1_kernel<<<grid, kWarpsO1 * 32, kO1Smem, st>>>(o);
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "overlap_o1 launch");
   cudaFreeAsync(dtiles, st);
   cudaFreeAsync(kmax, st);
-  if (!same) cudaFreeAsync(ket, st);
+  cudaFreeAsync(ket, st);
   cudaFreeAsync(bra, st);
   return MPSKQ_OK;
 }

@@ -493,6 +493,16 @@ extern "C" int mpskq_gram_host(int kind, int m, int r, int d, double gamma, doub
   if (!train) ST(check_rows_host(X_kets, n_kets, m));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t n_all = train ? n_bras : n_bras + n_kets;
+  {
+    // keep the stream-ordered pool's pages between calls (default threshold 0
+    // returns them to the driver at every synchronize)
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
 
   std::vector<int32_t> ops;
   int64_t n_gates = 0;
