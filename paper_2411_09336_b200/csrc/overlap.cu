@@ -58,23 +58,6 @@ __global__ void pack_o1_kernel(const double2* __restrict__ sites, const int32_t*
   }
 }
 
-// per 32-state block and bond: max bond dim over the block
-__global__ void block_max_chi_kernel(const int32_t* __restrict__ chi, int m, int64_t n,
-                                     int64_t nblk, int32_t* __restrict__ out) {
-  const int64_t total = nblk * (m + 1);
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t blk = idx / (m + 1);
-    const int b = (int)(idx % (m + 1));
-    int mx = 1;
-    for (int l = 0; l < kLanes; ++l) {
-      const int64_t s = blk * kLanes + l;
-      if (s < n) mx = max(mx, chi[s * (m + 1) + b]);
-    }
-    out[idx] = mx;
-  }
-}
-
 __device__ __forceinline__ void store_result(int out_mode, double* out, int64_t ld, int64_t i,
                                              int64_t j, double2 ov, bool mirror) {
   if (out_mode == MPSKQ_OUT_KERNEL) {
@@ -110,16 +93,18 @@ __global__ void pack_bra_kernel(const double2* __restrict__ sites, const int32_t
   }
 }
 
-constexpr int kStages = 4;
+constexpr int kStages = 8;  // power of two: ring index = counter & 7
 constexpr uint32_t kKetBytes = kEnt * kLanes * sizeof(double2);   // 16 KB per site
 constexpr uint32_t kBraBytes = kWarpsO1 * kEnt * sizeof(double2);  // 4 KB per site
-constexpr size_t kO1Smem = kStages * (size_t)(kKetBytes + kBraBytes) + kStages * sizeof(uint64_t);
+inline size_t o1_smem_bytes(int m) {
+  return kStages * (size_t)(kKetBytes + kBraBytes) + 2 * kStages * sizeof(uint64_t) + 16 +
+         sizeof(int32_t) * kWarpsO1 * (size_t)(m + 1);
+}
 
 struct O1Args {
   const double2* bra;  // [site][n_pad_bra][entry]
   const double2* ket;  // [site][nblk_ket][entry][lane]
   const int32_t* bra_chi;
-  const int32_t* ket_bmax;
   int64_t n_bras, n_kets, n_pad_bra, nblk_ket;
   int m, kind, out_mode;
   const int2* tiles;  // (bra tile of 8, ket block of 32)
@@ -128,114 +113,195 @@ struct O1Args {
   int64_t ld;
 };
 
+// Site step of one (bra, ket) pair, in two halves with many independent
+// accumulators (the FP64 pipe needs ILP: two warps per scheduler at ~220
+// registers) and a small code footprint (the whole kernel stays in the
+// instruction cache although the 8 warps run different bra shapes):
+//   phase 1  T[al][p][br] = sum_kb env[al][kb] B[kb][p][br]     al < NA (template)
+//   phase 2  env'[ar][br] = sum_{al,p} conj(A[al][p][ar]) T[al][p][br]
+//            in al blocks guarded by the bra's chi_s; ar runs over 2 or 4 rows
+//            (the bra's chi_{s+1} <= 2 or not)
+// The bra's bond dims are exact (warp-uniform); kb/br run over the zero-padded
+// 4 because the 32 kets of a warp rarely share a smaller bound.
+template <int NA>
+__device__ __forceinline__ void o1_phase1(const double2 (&env)[kP][kP], const double2* B,
+                                          double2 (&T)[kP][2][kP]) {
+#pragma unroll
+  for (int al = 0; al < NA; ++al)
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+      for (int br = 0; br < kP; ++br) T[al][p][br] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int kb = 0; kb < kP; ++kb) {
+    double2 b[2][kP];
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+      for (int br = 0; br < kP; ++br) b[p][br] = B[((kb * 2 + p) * kP + br) * kLanes];
+#pragma unroll
+    for (int al = 0; al < NA; ++al)
+#pragma unroll
+      for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int br = 0; br < kP; ++br) T[al][p][br] = cfma(env[al][kb], b[p][br], T[al][p][br]);
+  }
+}
+
+template <int R0, int NR>
+__device__ __forceinline__ void o1_phase2_rows(const double2* Aal, const double2 (&T)[kP][2][kP],
+                                               double2 (&env)[kP][kP]) {
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    double2 av[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) av[r] = Aal[p * kP + R0 + r];
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+      for (int br = 0; br < kP; ++br) env[R0 + r][br] = cfmac(av[r], T[0][p][br], env[R0 + r][br]);
+  }
+}
+
+template <int AL, int R0, int NR>
+__device__ __forceinline__ void o1_phase2_rows(const double2* A, const double2 (&T)[kP][2][kP],
+                                               double2 (&env)[kP][kP]) {
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    double2 av[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) av[r] = A[(AL * 2 + p) * kP + R0 + r];
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+      for (int br = 0; br < kP; ++br) env[R0 + r][br] = cfmac(av[r], T[AL][p][br], env[R0 + r][br]);
+  }
+}
+
+template <int AL>
+__device__ __forceinline__ void o1_phase2_al(const double2* A, const double2 (&T)[kP][2][kP], bool wide,
+                                             double2 (&env)[kP][kP]) {
+  o1_phase2_rows<AL, 0, 2>(A, T, env);
+  if (wide) o1_phase2_rows<AL, 2, 2>(A, T, env);
+}
+
+__device__ __forceinline__ void o1_phase2(const double2* A, const double2 (&T)[kP][2][kP], int na, int na1,
+                                          double2 (&env)[kP][kP]) {
+#pragma unroll
+  for (int ar = 0; ar < kP; ++ar)
+#pragma unroll
+    for (int br = 0; br < kP; ++br) env[ar][br] = make_double2(0.0, 0.0);
+  const bool wide = na1 > 2;
+  o1_phase2_al<0>(A, T, wide, env);
+  if (na > 1) o1_phase2_al<1>(A, T, wide, env);
+  if (na > 2) o1_phase2_al<2>(A, T, wide, env);
+  if (na > 3) o1_phase2_al<3>(A, T, wide, env);
+}
+
 // One CTA = 8 bras (warps) x 32 kets (lanes); one thread owns one pair's 4x4
-// complex environment in registers.  Thread 0 streams each site's ket block
-// (16 KB) and bra tile (4 KB) into a 4-stage shared-memory ring with TMA bulk
-// copies signalled on mbarriers, kStages-1 sites ahead of the compute.
+// complex environment in registers.  Persistent over its tiles, the CTA
+// streams each site's ket block (16 KB) and bra tile (4 KB) into a 6-stage
+// shared-memory ring with TMA bulk copies (cp.async.bulk) completing on
+// "full" mbarriers; every warp releases a slot on its "empty" mbarrier, so
+// warps drift up to the ring depth instead of synchronising every site.
+// Thread 0 is the producer: it refills opportunistically (test_wait) and
+// blocks only for the slot its own warp needs next (deadlock free).
 __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* sket = reinterpret_cast<double2*>(smem_raw);
   double2* sbra = sket + kStages * kEnt * kLanes;
   uint64_t* full = reinterpret_cast<uint64_t*>(sbra + kStages * kWarpsO1 * kEnt);
+  uint64_t* empty = full + kStages;
+  uint32_t* ld_ctr = reinterpret_cast<uint32_t*>(empty + kStages);  // sites issued so far
+  int32_t* schi = reinterpret_cast<int32_t*>(ld_ctr + 4);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m = a.m;
   if (tid == 0) {
-    for (int q = 0; q < kStages; ++q) mbar_init(&full[q], 1);
+    for (int q = 0; q < kStages; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], kWarpsO1);
+    }
+    *ld_ctr = 0;
     mbar_fence_init();
   }
   __syncthreads();
+  if ((int64_t)blockIdx.x >= a.n_tiles) return;
+  const int64_t my_tiles = (a.n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  const uint32_t total = (uint32_t)(my_tiles * m);
   const int64_t kstride = a.nblk_ket * kEnt * kLanes;  // per site
   const int64_t bstride = a.n_pad_bra * kEnt;
-  uint32_t it = 0;  // sites consumed by this CTA so far (ring position + phase)
-  for (int64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
-    const int2 tile = a.tiles[t];
-    const double2* kbase = a.ket + (int64_t)tile.y * kEnt * kLanes;
-    const double2* bbase = a.bra + (int64_t)tile.x * kWarpsO1 * kEnt;
-    auto issue = [&](int site, uint32_t q) {
-      const uint32_t buf = q % kStages;
-      mbar_arrive_expect_tx(&full[buf], kKetBytes + kBraBytes);
-      bulk_g2s(sket + buf * kEnt * kLanes, kbase + site * kstride, kKetBytes, &full[buf]);
-      bulk_g2s(sbra + buf * kWarpsO1 * kEnt, bbase + site * bstride, kBraBytes, &full[buf]);
-    };
-    if (tid == 0)
-      for (int s = 0; s < kStages - 1 && s < m; ++s) issue(s, it + s);
-
+  uint32_t it = 0;  // sites this warp consumed (ring position + phase)
+  auto issue = [&](uint32_t q) {
+    const int2 tl = a.tiles[blockIdx.x + (int64_t)(q / m) * gridDim.x];
+    const int site = (int)(q % m);
+    const uint32_t buf = q & (kStages - 1);
+    mbar_arrive_expect_tx(&full[buf], kKetBytes + kBraBytes);
+    bulk_g2s(sket + buf * kEnt * kLanes, a.ket + (int64_t)tl.y * kEnt * kLanes + site * kstride,
+             kKetBytes, &full[buf]);
+    bulk_g2s(sbra + buf * kWarpsO1 * kEnt, a.bra + (int64_t)tl.x * kWarpsO1 * kEnt + site * bstride,
+             kBraBytes, &full[buf]);
+  };
+  // Lane 0 of every warp produces: refill free slots opportunistically (the
+  // fastest warp keeps the ring full) and block only for the slot this warp
+  // needs next; a CAS on the shared counter issues every site exactly once.
+  // Warp-collective (all lanes take the same path; only the CAS and the
+  // copy issue are lane 0's), so the warp never leaves the producer diverged.
+  volatile uint32_t* vld = ld_ctr;
+  auto produce = [&]() {
+    for (;;) {
+      const uint32_t q = __shfl_sync(kFull, lane == 0 ? *vld : 0u, 0);
+      if (q >= total || q >= it + kStages) break;
+      if (q >= kStages) {
+        const uint32_t par = ((q / kStages) - 1) & 1;
+        if (q <= it) {
+          mbar_wait(&empty[q & (kStages - 1)], par);
+        } else {
+          const int ok = __shfl_sync(kFull, (int)mbar_test(&empty[q & (kStages - 1)], par), 0);
+          if (!ok) break;
+        }
+      }
+      if (lane == 0 && atomicCAS(ld_ctr, q, q + 1) == q) issue(q);
+      __syncwarp();
+    }
+  };
+  int32_t* mychi = schi + warp * (m + 1);
+  for (int64_t k = 0; k < my_tiles; ++k) {
+    const int2 tile = a.tiles[blockIdx.x + k * gridDim.x];
     const int64_t i = (int64_t)tile.x * kWarpsO1 + warp;  // bra (warp-uniform)
     const int64_t j = (int64_t)tile.y * kLanes + lane;    // ket (per lane)
     const int64_t ic = i < a.n_bras ? i : a.n_bras - 1;
-    const int32_t* bchi = a.bra_chi + ic * (m + 1);
-    const int32_t* kmax = a.ket_bmax + (int64_t)tile.y * (m + 1);
-
+    for (int b = lane; b <= m; b += kLanes) mychi[b] = __ldg(a.bra_chi + ic * (m + 1) + b);
+    __syncwarp();
     double2 env[kP][kP];
 #pragma unroll
     for (int x = 0; x < kP; ++x)
 #pragma unroll
       for (int y = 0; y < kP; ++y) env[x][y] = make_double2(x == 0 && y == 0 ? 1.0 : 0.0, 0.0);
-    int na = 1, nb = 1;  // chi_s of the bra / of the ket block
+    int na = 1;  // chi_s of the bra (warp-uniform)
     for (int s = 0; s < m; ++s) {
-      if (tid == 0 && s + kStages - 1 < m) issue(s + kStages - 1, it + kStages - 1);
-      const int na1 = __ldg(bchi + s + 1);
-      const int nb1 = __ldg(kmax + s + 1);
-      const uint32_t buf = it % kStages;
+      produce();
+      const int na1 = mychi[s + 1];
+      const uint32_t buf = it & (kStages - 1);
       mbar_wait(&full[buf], (it / kStages) & 1);
-      ++it;
       const double2* B = sket + buf * kEnt * kLanes + lane;  // B[e] at B[e * 32]
       const double2* A = sbra + buf * kWarpsO1 * kEnt + warp * kEnt;
-      double2 nenv[kP][kP];
-#pragma unroll
-      for (int x = 0; x < kP; ++x)
-#pragma unroll
-        for (int y = 0; y < kP; ++y) nenv[x][y] = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int br = 0; br < kP; ++br) {
-        if (br < nb1) {
-          double2 Bc[kP][2];  // column br of the ket tensor: B[kb][p][br]
-#pragma unroll
-          for (int kb = 0; kb < kP; ++kb)
-#pragma unroll
-            for (int p = 0; p < 2; ++p)
-              Bc[kb][p] = kb < nb ? B[((kb * 2 + p) * kP + br) * kLanes] : make_double2(0.0, 0.0);
-          // T[al][p] = sum_kb env[al][kb] B[kb][p][br]
-          double2 T[kP][2];
-#pragma unroll
-          for (int al = 0; al < kP; ++al)
-#pragma unroll
-            for (int p = 0; p < 2; ++p) {
-              double2 acc = make_double2(0.0, 0.0);
-              if (al < na) {
-#pragma unroll
-                for (int kb = 0; kb < kP; ++kb)
-                  if (kb < nb) acc = cfma(env[al][kb], Bc[kb][p], acc);
-              }
-              T[al][p] = acc;
-            }
-          // nenv[ar][br] = sum_{al,p} conj(A[al][p][ar]) T[al][p]  (two partial chains)
-#pragma unroll
-          for (int ar = 0; ar < kP; ++ar) {
-            if (ar < na1) {
-              double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
-#pragma unroll
-              for (int al = 0; al < kP; ++al)
-                if (al < na) {
-                  acc0 = cfmac(A[(al * 2 + 0) * kP + ar], T[al][0], acc0);
-                  acc1 = cfmac(A[(al * 2 + 1) * kP + ar], T[al][1], acc1);
-                }
-              nenv[ar][br] = cadd(acc0, acc1);
-            }
-          }
-        }
+      double2 T[kP][2][kP];
+      switch (na) {
+        case 1: o1_phase1<1>(env, B, T); break;
+        case 2: o1_phase1<2>(env, B, T); break;
+        case 3: o1_phase1<3>(env, B, T); break;
+        default: o1_phase1<4>(env, B, T); break;
       }
-#pragma unroll
-      for (int x = 0; x < kP; ++x)
-#pragma unroll
-        for (int y = 0; y < kP; ++y) env[x][y] = nenv[x][y];
+      o1_phase2(A, T, na, na1, env);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[buf]);
+      ++it;
       na = na1;
-      nb = nb1;
-      __syncthreads();  // every warp is done with `buf` before it is refilled
     }
     const bool train = a.kind == MPSKQ_KIND_TRAIN;
     const bool valid = i < a.n_bras && j < a.n_kets && (!train || i < j);
     if (valid) store_result(a.out_mode, a.out, a.ld, i, j, env[0][0], train);
+    __syncwarp();
   }
 }
 
@@ -365,13 +431,11 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
   const int64_t nbk = (a.n_kets + kLanes - 1) / kLanes;
   const size_t bb = sizeof(double2) * (size_t)m * npb * kEnt;
   const size_t kb = sizeof(double2) * (size_t)m * nbk * kEnt * kLanes;
-  void *bra = nullptr, *ket = nullptr, *kmax = nullptr;
+  void *bra = nullptr, *ket = nullptr;
   cudaError_t e = cudaMallocAsync(&bra, bb, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(packed bras)");
   e = cudaMallocAsync(&ket, kb, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(packed kets)");
-  e = cudaMallocAsync(&kmax, sizeof(int32_t) * nbk * (m + 1), st);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(block chi)");
   const int threads = 256;
   auto blocks_for = [&](int64_t total) {
     return (int)std::min<int64_t>((total + threads - 1) / threads, 148 * 64);
@@ -382,34 +446,27 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
   pack_o1_kernel<<<blocks_for((int64_t)m * nbk * kEnt * kLanes), threads, 0, st>>>(
       reinterpret_cast<const double2*>(a.ket_sites), a.ket_chi, a.site_off, a.state_stride, m,
       a.n_kets, nbk, static_cast<double2*>(ket));
-  block_max_chi_kernel<<<blocks_for(nbk * (m + 1)), threads, 0, st>>>(a.ket_chi, m, a.n_kets, nbk,
-                                                                      static_cast<int32_t*>(kmax));
   const bool train = a.kind == MPSKQ_KIND_TRAIN;
   auto tiles = make_tiles(train, a.n_bras, a.n_kets, kWarpsO1, kLanes, a.rank, a.world);
   int2* dtiles = nullptr;
   if (int s = upload_tiles(tiles, &dtiles, st)) return s;
   if (!tiles.empty()) {
-    static bool attr = false;
-    if (!attr) {
-      e = cudaFuncSetAttribute(overlap_o1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kO1Smem);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(o1)");
-      attr = true;
-    }
+    const size_t smem = o1_smem_bytes(m);
+    e = cudaFuncSetAttribute(overlap_o1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(o1)");
     O1Args o{static_cast<const double2*>(bra), static_cast<const double2*>(ket), a.bra_chi,
-             static_cast<const int32_t*>(kmax), a.n_bras, a.n_kets, npb, nbk, m, a.kind,
+             a.n_bras, a.n_kets, npb, nbk, m, a.kind,
              a.out_mode, dtiles, (int64_t)tiles.size(), a.out, a.ld};
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // persistent: one CTA per SM walks the tile list (the ring stays warm)
     const int grid = (int)std::min<int64_t>((int64_t)tiles.size(), sms);
-    overlap_o1_kernel<<<grid, kWarpsO1 * 32, kO1Smem, st>>>(o);
+    overlap_o1_kernel<<<grid, kWarpsO1 * 32, smem, st>>>(o);
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "overlap_o1 launch");
   cudaFreeAsync(dtiles, st);
-  cudaFreeAsync(kmax, st);
   cudaFreeAsync(ket, st);
   cudaFreeAsync(bra, st);
   return MPSKQ_OK;
