@@ -401,17 +401,25 @@ int upload_tiles(const std::vector<int2>& tiles, int2** dev, cudaStream_t st) {
 }
 
 // tiles of (row block of rb rows, column block of cb columns); train keeps
-// the tiles holding some i < j.  Block-cyclic: tile t goes to rank t % world.
+// the tiles holding some i < j.  Tiles are enumerated super-block by
+// super-block (about 384 bras x 384 kets each) so the tiles that run
+// concurrently on the 148 SMs share their bra and ket site data in L2.
+// Block-cyclic over ranks: tile t goes to rank t % world.
 std::vector<int2> make_tiles(bool train, int64_t n_rows, int64_t n_cols, int rb, int cb, int rank,
                              int world) {
   std::vector<int2> tiles;
   const int64_t nrb = (n_rows + rb - 1) / rb, ncb = (n_cols + cb - 1) / cb;
+  const int64_t sr = std::max<int64_t>(1, 384 / rb), sc = std::max<int64_t>(1, 384 / cb);
   int64_t t = 0;
-  for (int64_t J = 0; J < ncb; ++J) {
-    const int64_t jmax = std::min(n_cols, (J + 1) * cb) - 1;
-    for (int64_t I = 0; I < nrb; ++I) {
-      if (train && I * rb >= jmax) break;
-      if (t++ % world == rank) tiles.push_back(make_int2((int)I, (int)J));
+  for (int64_t J0 = 0; J0 < ncb; J0 += sc) {
+    for (int64_t I0 = 0; I0 < nrb; I0 += sr) {
+      for (int64_t J = J0; J < std::min(ncb, J0 + sc); ++J) {
+        const int64_t jmax = std::min(n_cols, (J + 1) * cb) - 1;
+        for (int64_t I = I0; I < std::min(nrb, I0 + sr); ++I) {
+          if (train && I * rb >= jmax) break;
+          if (t++ % world == rank) tiles.push_back(make_int2((int)I, (int)J));
+        }
+      }
     }
   }
   return tiles;

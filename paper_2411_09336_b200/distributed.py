@@ -39,16 +39,42 @@ def shard(n: int, world: int, rank: int) -> tuple:
     return lo, lo + q + (rank < rem)
 
 
+def _host_collectives(group=None) -> bool:
+    """gloo runs the collectives on host copies (tests / CPU); NCCL on device."""
+    import torch.distributed as dist
+
+    return dist.get_backend(group) == "gloo"
+
+
 def allgather_rows(local: torch.Tensor, counts: list, group=None) -> torch.Tensor:
     """Concatenate every rank's rows (ragged along dim 0) on every rank."""
     import torch.distributed as dist
 
+    dev = local.device
+    if _host_collectives(group):
+        local = local.cpu()
     mx = max(counts)
     pad = local.new_zeros((mx,) + tuple(local.shape[1:]))
     pad[: local.shape[0]] = local
     parts = [torch.empty_like(pad) for _ in counts]
     dist.all_gather(parts, pad, group=group)
-    return torch.cat([p[:c] for p, c in zip(parts, counts)], dim=0)
+    return torch.cat([p[:c] for p, c in zip(parts, counts)], dim=0).to(dev)
+
+
+def _all_reduce_max(t: torch.Tensor, group=None) -> torch.Tensor:
+    import torch.distributed as dist
+
+    h = t.cpu() if _host_collectives(group) else t
+    dist.all_reduce(h, op=dist.ReduceOp.MAX, group=group)
+    return h.to(t.device)
+
+
+def _reduce_sum_to0(t: torch.Tensor, group=None) -> torch.Tensor:
+    import torch.distributed as dist
+
+    h = t.cpu() if _host_collectives(group) else t
+    dist.reduce(h, dst=0, op=dist.ReduceOp.SUM, group=group)
+    return h.to(t.device)
 
 
 def tiles_of(kind: str, chi_cap: int, n_bras: int, n_kets: int, rank: int, world: int) -> tuple:
@@ -85,8 +111,7 @@ def gram(X_bras, X_kets, cfg, kind: str, budget: float, chi_max: int = 0, group=
         local = simulate_rows(X_all[lo:hi], cfg, budget, chi_max) if hi > lo else None
         if world > 1:
             cap = torch.tensor([local.chi_cap if local is not None else 0], device="cuda")
-            dist.all_reduce(cap, op=dist.ReduceOp.MAX, group=group)
-            cap = int(cap.item())
+            cap = int(_all_reduce_max(cap, group).item())
             if local is not None and local.chi_cap != cap:
                 local = simulate_rows(X_all[lo:hi], cfg, budget, chi_max, chi_cap=cap)
     rep.n_simulations = n_all
@@ -122,7 +147,7 @@ def gram(X_bras, X_kets, cfg, kind: str, budget: float, chi_max: int = 0, group=
         overlap_matrix(bras, kets, kind, rank=rank, world=world, out=K_dev)
     t0 = time.perf_counter()
     if world > 1:
-        dist.reduce(K_dev, dst=0, op=dist.ReduceOp.SUM, group=group)
+        K_dev = _reduce_sum_to0(K_dev, group)
     K = K_dev.cpu().numpy() if rank == 0 else np.empty((0, 0))
     rep._add("simulation", t_sim.seconds())
     rep._add("inner_products", t_ov.seconds())

@@ -1,0 +1,65 @@
+"""run_distributed over 2 processes sharing one GPU (gloo collectives on host
+copies; the ranks' kernels never wait on each other): the sharded
+simulation, ragged all-gather, block-cyclic tile split and SUM-reduce must
+reproduce the single-process kernel matrix bitwise."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _rank(rank, world, port, kind, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2411_09336_b200 as P
+
+        torch.cuda.set_device(0)
+        g = golden("headline_m165_d1.npz")
+        cfg = P.FeatureMapConfig(165, 2, 1, 0.1)
+        Xb = g["X"] if kind == "train" else g["X_test"]
+        sched = P.make_schedule(len(Xb), len(g["X"]), world, "round_robin", kind)
+        rep = P.RunReport()
+        K = P.run_distributed(Xb, g["X"], cfg, sched, budget=1e-24, report=rep).entries
+        q.put((rank, K, rep.n_simulations, rep.n_inner_products))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["train", "test"])
+def test_two_ranks_on_one_gpu_match_single_process(kind):
+    import paper_2411_09336_b200 as P
+
+    g = golden("headline_m165_d1.npz")
+    cfg = P.FeatureMapConfig(165, 2, 1, 0.1)
+    Xb = g["X"] if kind == "train" else g["X_test"]
+    ref = P.run_distributed(Xb, g["X"], cfg, P.make_schedule(len(Xb), len(g["X"]), 1, "round_robin", kind)).entries
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, kind, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict((r, (K, ns, ni)) for r, K, ns, ni in (q.get(timeout=300) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    K0 = out[0][0]
+    assert np.array_equal(K0, ref)
+    assert np.abs(K0 - (g["K_train"] if kind == "train" else g["K_test"])).max() < 1e-10
