@@ -39,8 +39,10 @@ from .mps import (
     MpsBatch,
     MpsState,
     SimStats,
+    deserialize_state,
     init_state,
     inner_product,
+    serialize_state,
     simulate_circuit,
     stats,
     to_statevector,

@@ -247,9 +247,11 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
   // Warp-collective (all lanes take the same path; only the CAS and the
   // copy issue are lane 0's), so the warp never leaves the producer diverged.
   volatile uint32_t* vld = ld_ctr;
+  uint32_t seen = 0;  // last issue count this warp observed (warp-uniform)
   auto produce = [&]() {
     for (;;) {
       const uint32_t q = __shfl_sync(kFull, lane == 0 ? *vld : 0u, 0);
+      seen = q;
       if (q >= total || q >= it + kStages) break;
       if (q >= kStages) {
         const uint32_t par = ((q / kStages) - 1) & 1;
@@ -279,7 +281,9 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
       for (int y = 0; y < kP; ++y) env[x][y] = make_double2(x == 0 && y == 0 ? 1.0 : 0.0, 0.0);
     int na = 1;  // chi_s of the bra (warp-uniform)
     for (int s = 0; s < m; ++s) {
-      produce();
+      // the counter only grows: run the producer when this warp's view of the
+      // ring is less than half full (or its next slot may not be issued yet)
+      if (seen < it + kStages / 2 + 1 && seen < total) produce();
       const int na1 = mychi[s + 1];
       const uint32_t buf = it & (kStages - 1);
       mbar_wait(&full[buf], (it / kStages) & 1);

@@ -108,23 +108,26 @@ __device__ void apply_reflector(double2* M, const double2* u, double tau, int j,
     const int c = c0 + (act ? ci : 0);
     double2 acc = cz();
     if (act)
+      #pragma unroll 1
       for (int r = j + g; r < Rr; r += G) acc = cfmac(u[r], M[c * LD + r], acc);
     acc = group_sum(acc, G);
     if (act) {
       const double2 w = cscale(acc, tau);
+      #pragma unroll 1
       for (int r = j + g; r < Rr; r += G) M[c * LD + r] = csub(M[c * LD + r], cmul(u[r], w));
     }
   }
 }
 
 template <int CAP, int NT>
-__device__ int householder_qr(Smem<CAP, NT>& sm, int Rr, int Cc) {
+__device__ __noinline__ int householder_qr(Smem<CAP, NT>& sm, int Rr, int Cc) {
   constexpr int LD = 2 * CAP;
   const int tid = threadIdx.x;
   const int k = min(Rr, Cc);
   double2* A = sm.A;
   for (int j = 0; j < k; ++j) {
     double part = 0.0;
+    #pragma unroll 1
     for (int r = j + tid; r < Rr; r += NT) part += cnorm2(A[j * LD + r]);
     const double nx2 = block_sum<NT>(part, sm.red);
     if (tid == 0) {
@@ -146,6 +149,7 @@ __device__ int householder_qr(Smem<CAP, NT>& sm, int Rr, int Cc) {
     bsync<NT>();
   }
   // Q = H_0 ... H_{k-1} [I_k; 0]
+  #pragma unroll 1
   for (int idx = tid; idx < Rr * k; idx += NT) {
     const int c = idx / Rr, r = idx % Rr;
     sm.W[c * LD + r] = make_double2(r == c ? 1.0 : 0.0, 0.0);
@@ -168,32 +172,38 @@ __device__ __forceinline__ double2 r_entry(const Smem<CAP, NT>& sm, int kk, int 
 // ---------------------------------------------------------------------------
 // One-sided Jacobi on C (Rr x n, column-major in A) accumulating the unitary
 // W (n x n) with C_out = C_in W and mutually orthogonal columns of C_out.
-template <int CAP, int NT>
-__device__ void jacobi(Smem<CAP, NT>& sm, int Rr, int n) {
+// Column pairs follow the circle-method round robin (n/2 disjoint pairs per
+// round, ne-1 rounds per sweep), one group of G lanes per pair.
+template <int G>
+__device__ __forceinline__ double gsum(double v) {
+#pragma unroll
+  for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+template <int CAP, int NT, int G>
+__device__ __noinline__ void jacobi_sweeps(Smem<CAP, NT>& sm, int Rr, int n) {
   constexpr int LD = 2 * CAP;
   const int tid = threadIdx.x;
   double2* A = sm.A;
   double2* W = sm.W;
-  for (int idx = tid; idx < n * n; idx += NT) {
-    const int c = idx / n, r = idx % n;
-    W[c * LD + r] = make_double2(r == c ? 1.0 : 0.0, 0.0);
-  }
-  bsync<NT>();
-  if (n < 2) return;
-  const int ne = n + (n & 1);
-  const int P = ne >> 1;
-  const int G = group_width<NT>(P);
+  const int ne = n + (n & 1), P = ne >> 1, span = ne - 1;
   const int k = tid / G, g = tid % G;
+  // convergence: |c_p^H c_q| <= tol * |c_p| |c_q|, compared in squares
   const double tol = DBL_EPSILON * (double)max(Rr, 8);
+  const double tol2 = tol * tol;
   for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
     int rotated = 0;
-    for (int t = 0; t < ne - 1; ++t) {
-      // circle-method tournament: positions (k, ne-1-k)
-      int p = -1, q = -1;
+    for (int t = 0; t < span; ++t) {
+      // circle method: position 0 is fixed, positions 1..ne-1 rotate by t
+      int p = 0, q = 0;
       if (k < P) {
         const int pa = k, pb = ne - 1 - k;
-        p = pa == 0 ? 0 : 1 + (pa - 1 + t) % (ne - 1);
-        q = pb == 0 ? 0 : 1 + (pb - 1 + t) % (ne - 1);
+        int x = pa - 1 + t, y = pb - 1 + t;
+        x = x >= span ? x - span : x;
+        y = y >= span ? y - span : y;
+        p = pa == 0 ? 0 : 1 + x;
+        q = 1 + y;
         if (p > q) {
           const int tmp = p;
           p = q;
@@ -201,44 +211,44 @@ __device__ void jacobi(Smem<CAP, NT>& sm, int Rr, int n) {
         }
       }
       const bool act = k < P && q < n;
-      double a = 0.0, b = 0.0;
-      double2 gm = cz();
+      double a = 0.0, b = 0.0, gx = 0.0, gy = 0.0;
       if (act) {
+        #pragma unroll 1
         for (int r = g; r < Rr; r += G) {
           const double2 x = A[p * LD + r], y = A[q * LD + r];
-          a += cnorm2(x);
-          b += cnorm2(y);
-          gm = cfmac(x, y, gm);
+          a = fma(x.x, x.x, fma(x.y, x.y, a));
+          b = fma(y.x, y.x, fma(y.y, y.y, b));
+          gx = fma(x.x, y.x, fma(x.y, y.y, gx));
+          gy = fma(x.x, y.y, fma(-x.y, y.x, gy));
         }
       }
-      a = group_sum(a, G);
-      b = group_sum(b, G);
-      gm = group_sum(gm, G);
-      if (act) {
-        const double ag = hypot(gm.x, gm.y);
-        if (ag > tol * sqrt(a) * sqrt(b) && ag > 0.0) {
-          rotated = 1;
-          const double zeta = (b - a) / (2.0 * ag);
-          double t_;
-          if (fabs(zeta) > 1e150)
-            t_ = 0.5 / zeta;
-          else
-            t_ = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = 1.0 / sqrt(1.0 + t_ * t_);
-          const double s = c * t_;
-          const double2 e = make_double2(gm.x / ag, gm.y / ag);
-          // [x', y'] = [x, y] J,  J = [[c, s e], [-s conj(e), c]]
-          const double2 se = cscale(e, s);
-          for (int r = g; r < Rr; r += G) {
-            const double2 x = A[p * LD + r], y = A[q * LD + r];
-            A[p * LD + r] = csub(cscale(x, c), cmul(cconj(se), y));
-            A[q * LD + r] = cadd(cmul(se, x), cscale(y, c));
-          }
-          for (int r = g; r < n; r += G) {
-            const double2 x = W[p * LD + r], y = W[q * LD + r];
-            W[p * LD + r] = csub(cscale(x, c), cmul(cconj(se), y));
-            W[q * LD + r] = cadd(cmul(se, x), cscale(y, c));
-          }
+      a = gsum<G>(a);
+      b = gsum<G>(b);
+      gx = gsum<G>(gx);
+      gy = gsum<G>(gy);
+      const double g2 = fma(gx, gx, gy * gy);
+      if (act && g2 > tol2 * a * b && g2 > 0.0) {
+        rotated = 1;
+        const double inv = rsqrt(g2);  // 1/|gamma|
+        const double zeta = (b - a) * (0.5 * inv);
+        const double az = fabs(zeta);
+        const double tt = az > 1e150 ? 0.5 / az : 1.0 / (az + sqrt(fma(zeta, zeta, 1.0)));
+        const double t_ = copysign(tt, zeta);
+        const double c = rsqrt(fma(t_, t_, 1.0));
+        const double sn = c * t_;
+        // [x', y'] = [x, y] J,  J = [[c, s e], [-s conj(e), c]],  e = gamma/|gamma|
+        const double2 se = make_double2(sn * gx * inv, sn * gy * inv);
+        #pragma unroll 1
+        for (int r = g; r < Rr; r += G) {
+          const double2 x = A[p * LD + r], y = A[q * LD + r];
+          A[p * LD + r] = csub(cscale(x, c), cmul(cconj(se), y));
+          A[q * LD + r] = cadd(cmul(se, x), cscale(y, c));
+        }
+        #pragma unroll 1
+        for (int r = g; r < n; r += G) {
+          const double2 x = W[p * LD + r], y = W[q * LD + r];
+          W[p * LD + r] = csub(cscale(x, c), cmul(cconj(se), y));
+          W[q * LD + r] = cadd(cmul(se, x), cscale(y, c));
         }
       }
       bsync<NT>();
@@ -247,9 +257,31 @@ __device__ void jacobi(Smem<CAP, NT>& sm, int Rr, int n) {
   }
 }
 
+template <int CAP, int NT>
+__device__ void jacobi(Smem<CAP, NT>& sm, int Rr, int n) {
+  constexpr int LD = 2 * CAP;
+  const int tid = threadIdx.x;
+  #pragma unroll 1
+  for (int idx = tid; idx < n * n; idx += NT) {
+    const int c = idx / n, r = idx - c * n;
+    sm.W[c * LD + r] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+  }
+  bsync<NT>();
+  if (n < 2) return;
+  // lanes per column pair: G * (n/2) <= NT, G in {8, 16, 32} for every
+  // (CAP, NT) instantiation (NT >= 8 * CAP)
+  const int G = group_width<NT>((n + 1) >> 1);
+  if (G >= 32)
+    jacobi_sweeps<CAP, NT, 32>(sm, Rr, n);
+  else if (G == 16)
+    jacobi_sweeps<CAP, NT, 16>(sm, Rr, n);
+  else
+    jacobi_sweeps<CAP, NT, 8>(sm, Rr, n);
+}
+
 // column norms of C, descending order in perm (ties keep index order)
 template <int CAP, int NT>
-__device__ void norms_and_order(Smem<CAP, NT>& sm, int Rr, int n) {
+__device__ __noinline__ void norms_and_order(Smem<CAP, NT>& sm, int Rr, int n) {
   constexpr int LD = 2 * CAP;
   const int tid = threadIdx.x;
   const int G = group_width<NT>(n);
@@ -258,11 +290,13 @@ __device__ void norms_and_order(Smem<CAP, NT>& sm, int Rr, int n) {
     const int c = base + tid / G, g = tid % G;
     double acc = 0.0;
     if (c < n)
+      #pragma unroll 1
       for (int r = g; r < Rr; r += G) acc += cnorm2(sm.A[c * LD + r]);
     acc = group_sum(acc, G);
     if (c < n && g == 0) sm.sig[c] = sqrt(acc);
   }
   bsync<NT>();
+  #pragma unroll 1
   for (int j = tid; j < n; j += NT) {
     const double sj = sm.sig[j];
     int rank = 0;
@@ -279,7 +313,7 @@ __device__ void norms_and_order(Smem<CAP, NT>& sm, int Rr, int n) {
 // plus the renormalisation factor of apply_two_qubit (mps.py:189-192).
 // Runs on one thread; writes keep to ibuf[0] and factor/discarded to scal[0..1].
 template <int CAP, int NT>
-__device__ void truncation_rule(Smem<CAP, NT>& sm, int kmin, double budget, int chi_max) {
+__device__ __noinline__ void truncation_rule(Smem<CAP, NT>& sm, int kmin, double budget, int chi_max) {
   double v[2 * CAP];
   const double s0 = sm.sig[sm.perm[0]];
   for (int i = 0; i < kmin; ++i) {
@@ -326,6 +360,7 @@ __device__ void op_one_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, d
   const int chl = sm.chi[q], chr = sm.chi[q + 1];
   double2* p = st.base + st.off[q];
   const int n = chl * chr;
+  #pragma unroll 1
   for (int idx = threadIdx.x; idx < n; idx += NT) {
     const int a = idx / chr, b = idx - a * chr;
     const int i0 = (2 * a) * chr + b, i1 = i0 + chr;
@@ -357,19 +392,23 @@ __device__ void op_qr_left(Smem<CAP, NT>& sm, StateCtx& st, int i) {
   double2* M = st.base + st.off[i];
   double2* N = st.base + st.off[i + 1];
   const int Rr = 2 * chl;
+  #pragma unroll 1
   for (int idx = tid; idx < Rr * chr; idx += NT) {
     const int r = idx / chr, c = idx - r * chr;
     sm.A[c * LD + r] = M[idx];
   }
   const int nn = chr * 2 * chn;
+  #pragma unroll 1
   for (int idx = tid; idx < nn; idx += NT) sm.S[idx] = N[idx];
   bsync<NT>();
   const int k = householder_qr<CAP, NT>(sm, Rr, chr);
+  #pragma unroll 1
   for (int idx = tid; idx < Rr * k; idx += NT) {
     const int r = idx / k, c = idx - r * k;
     M[idx] = sm.W[c * LD + r];
   }
   const int cols = 2 * chn;
+  #pragma unroll 1
   for (int idx = tid; idx < k * cols; idx += NT) {
     const int kk = idx / cols, col = idx - kk * cols;
     double2 acc = cz();
@@ -390,19 +429,23 @@ __device__ void op_qr_right(Smem<CAP, NT>& sm, StateCtx& st, int i) {
   double2* M = st.base + st.off[i];
   double2* P = st.base + st.off[i - 1];
   const int Rr = 2 * chr;  // rows of M^H
+  #pragma unroll 1
   for (int idx = tid; idx < chl * Rr; idx += NT) {
     const int c = idx / Rr, r = idx - c * Rr;
     sm.A[c * LD + r] = cconj(M[idx]);
   }
   const int np = 2 * chp * chl;
+  #pragma unroll 1
   for (int idx = tid; idx < np; idx += NT) sm.S[idx] = P[idx];
   bsync<NT>();
   const int k = householder_qr<CAP, NT>(sm, Rr, chl);
+  #pragma unroll 1
   for (int idx = tid; idx < k * Rr; idx += NT) {
     const int kk = idx / Rr, r = idx - kk * Rr;
     M[idx] = cconj(sm.W[kk * LD + r]);
   }
   const int rows = 2 * chp;
+  #pragma unroll 1
   for (int idx = tid; idx < rows * k; idx += NT) {
     const int row = idx / k, kk = idx - row * k;
     double2 acc = cz();
@@ -426,7 +469,9 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
   const int Mr = 2 * chl, Nc = 2 * chr;
   double2* Xs = sm.W;
   double2* Ys = sm.W + 2 * CAP * CAP;
+  #pragma unroll 1
   for (int idx = tid; idx < Mr * chm; idx += NT) Xs[idx] = X[idx];
+  #pragma unroll 1
   for (int idx = tid; idx < chm * Nc; idx += NT) Ys[idx] = Y[idx];
   bsync<NT>();
   // theta = site_q . site_{q+1} (mps.py:183), gate on the physical legs
@@ -434,6 +479,7 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
   const double c = cs.x, s = cs.y;
   const bool rxx = code == MPSKQ_OP_RXX;
   int bad = 0;
+  #pragma unroll 1
   for (int it = tid; it < chl * chr * 2; it += NT) {
     const int t = it & 1, lr = it >> 1;
     const int l = lr / chr, rr = lr - l * chr;
@@ -486,20 +532,24 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
   }
   if (left) {
     // site_q = U s (mps.py:194), site_{q+1} = Vh
+    #pragma unroll 1
     for (int idx = tid; idx < Mr * keep; idx += NT) {
       const int row = idx / keep, kk = idx - row * keep;
       X[idx] = cscale(sm.A[sm.perm[kk] * LD + row], factor);
     }
+    #pragma unroll 1
     for (int idx = tid; idx < keep * Nc; idx += NT) {
       const int kk = idx / Nc, col = idx - kk * Nc;
       Y[idx] = cconj(sm.W[sm.perm[kk] * LD + col]);
     }
   } else {
     // site_q = U, site_{q+1} = s Vh (mps.py:197-199)
+    #pragma unroll 1
     for (int idx = tid; idx < Mr * keep; idx += NT) {
       const int row = idx / keep, kk = idx - row * keep;
       X[idx] = sm.W[sm.perm[kk] * LD + row];
     }
+    #pragma unroll 1
     for (int idx = tid; idx < keep * Nc; idx += NT) {
       const int kk = idx / Nc, col = idx - kk * Nc;
       Y[idx] = cscale(cconj(sm.A[sm.perm[kk] * LD + col]), factor);
@@ -528,7 +578,9 @@ __global__ void __launch_bounds__(NT) sim_kernel(SimArgs a) {
     StateCtx st{reinterpret_cast<double2*>(a.sites) + n * a.state_stride, a.site_off, m,
                 MPSKQ_STATE_OK, 1, 0.0};
     // init_state(m, "zero"): every site (1, 2, 1) = [1, 0]  (mps.py:90-102)
+    #pragma unroll 1
     for (int b = tid; b <= m; b += NT) sm.chi[b] = 1;
+    #pragma unroll 1
     for (int s = tid; s < m; s += NT) {
       st.base[a.site_off[s]] = make_double2(1.0, 0.0);
       st.base[a.site_off[s] + 1] = cz();
@@ -562,6 +614,7 @@ __global__ void __launch_bounds__(NT) sim_kernel(SimArgs a) {
         a.entry_log[n * a.n_gates + op.w] = entries;
       }
     }
+    #pragma unroll 1
     for (int b = tid; b <= m; b += NT) a.chi[n * (m + 1) + b] = sm.chi[b];
     if (tid == 0) {
       a.discard[n] = st.discard;
@@ -584,6 +637,7 @@ __global__ void __launch_bounds__(NT) svd_kernel(SvdArgs a) {
   for (int64_t b = blockIdx.x; b < a.batch; b += gridDim.x) {
     const double2* M = reinterpret_cast<const double2*>(a.mats) + b * rows * cols;
     int bad = 0;
+    #pragma unroll 1
     for (int idx = tid; idx < rows * cols; idx += NT) {
       const int r = idx / cols, c = idx - r * cols;
       const double2 v = M[idx];
@@ -599,18 +653,21 @@ __global__ void __launch_bounds__(NT) svd_kernel(SvdArgs a) {
     if (tid == 0) truncation_rule<CAP, NT>(sm, kmin, a.budget, a.chi_max);
     bsync<NT>();
     const double s0 = sm.sig[sm.perm[0]];
+    #pragma unroll 1
     for (int k = tid; k < kmin; k += NT) {
       double x = sm.sig[sm.perm[k]];
       if (s0 > 0.0 && x < kNoiseFloor * s0) x = 0.0;
       a.s[b * kmin + k] = x;
     }
     double2* U = reinterpret_cast<double2*>(a.u) + b * rows * kmin;
+    #pragma unroll 1
     for (int idx = tid; idx < rows * kmin; idx += NT) {
       const int r = idx / kmin, k = idx - r * kmin;
       const double nrm = sm.sig[sm.perm[k]];
       U[idx] = nrm > 0.0 ? cscale(sm.A[sm.perm[k] * LD + r], 1.0 / nrm) : cz();
     }
     double2* Vh = reinterpret_cast<double2*>(a.vh) + b * kmin * cols;
+    #pragma unroll 1
     for (int idx = tid; idx < kmin * cols; idx += NT) {
       const int k = idx / cols, c = idx - k * cols;
       Vh[idx] = cconj(sm.W[sm.perm[k] * LD + c]);

@@ -15,6 +15,7 @@ Drop-in for the hot-path names of the reference's ``mpskernel.mps``
 from __future__ import annotations
 
 import functools
+import struct
 from collections.abc import Sequence
 from dataclasses import dataclass, field
 
@@ -100,6 +101,39 @@ def to_statevector(state: MpsState) -> np.ndarray:
     for t in state.sites:
         psi = np.einsum("xa,apb->xpb", psi, t).reshape(-1, t.shape[2])
     return psi.reshape(-1)
+
+
+# ---------------------------------------------------------------- wire format
+_MAGIC = b"MPS1"
+_HEADER = struct.Struct("<IddiIQQ")  # m, budget, discard, center, peak_chi, g1, g2
+
+
+def serialize_state(state: MpsState) -> bytes:
+    """MPS1 bytes (mps.py:294-314): header, then per site (chi_l, chi_r) as
+    <II and the little-endian complex128 entries."""
+    center = -1 if state.ortho_center is None else state.ortho_center
+    out = [_MAGIC, _HEADER.pack(state.m, state.trunc_budget_per_gate, state.accumulated_discard, center,
+                                state.peak_chi, state.gate_count_1q, state.gate_count_2q)]
+    for t in state.sites:
+        out.append(struct.pack("<II", t.shape[0], t.shape[2]))
+        out.append(np.ascontiguousarray(t, dtype="<c16").tobytes())
+    return b"".join(out)
+
+
+def deserialize_state(buf: bytes) -> MpsState:
+    """Inverse of serialize_state (mps.py:317-340)."""
+    if bytes(buf[:4]) != _MAGIC:
+        raise ValueError("not a serialized MPS state")
+    m, budget, disc, center, peak, g1, g2 = _HEADER.unpack_from(buf, 4)
+    off = 4 + _HEADER.size
+    sites = []
+    for _ in range(m):
+        cl, cr = struct.unpack_from("<II", buf, off)
+        off += 8
+        n = cl * 2 * cr
+        sites.append(np.frombuffer(buf, dtype="<c16", count=n, offset=off).astype(np.complex128).reshape(cl, 2, cr))
+        off += 16 * n
+    return MpsState(sites, budget, disc, None if center < 0 else center, peak, g1, g2)
 
 
 # ---------------------------------------------------------------- programs

@@ -206,3 +206,51 @@ if __name__ == "__main__":
     gram_case("config2_m50_d2", 50, 2, 2, 0.1, 1e-24, 24, 8, seed=0)
     # config 3 shape: m=100, d=4, fidelity cutoff 1e-16
     gram_case("config3_m100_d4", 100, 2, 4, 0.1, 1e-16, 10, 4, seed=0)
+
+
+def svc_experiment():
+    """Config 1's experiment flow (cli.cmd_experiment, cli.py:152-214): blobs ->
+    balanced split -> rescale -> train/test kernels -> SMO SVM over the C grid.
+    Records the reference's K and downstream metrics, plus sklearn's
+    precomputed-kernel SVC on the reference K (the GPU test reruns sklearn on
+    the GPU K and must reproduce these)."""
+    from mpskernel import cli, learn
+    from sklearn.svm import SVC
+
+    ds = cli.generate_blobs(cli.SyntheticSpec(n_per_class=40), m=8, seed=0)
+    train, test = learn.split(ds, 0.8, seed=0)
+    X_tr, X_te, _ = learn.rescale(train.features, test.features)
+    cfg = ansatz.FeatureMapConfig(8, 2, 1, 0.5)
+    gtr = kernel.run_distributed(X_tr, X_tr, cfg, kernel.make_schedule(len(X_tr), len(X_tr), 1, "round_robin", "train"), budget=0.0)
+    gte = kernel.run_distributed(X_te, X_tr, cfg, kernel.make_schedule(len(X_te), len(X_tr), 1, "round_robin", "test"), budget=0.0)
+    grid = np.geomspace(0.01, 4.0, 8)
+    ref_auc, ref_acc, sk_pred, sk_dec = [], [], [], []
+    for C in grid:
+        model = learn.svm_train(gtr, train.labels, float(C))
+        met = learn.evaluate(learn.decision_scores(model, gte), test.labels)
+        ref_auc.append(met.auc)
+        ref_acc.append(met.accuracy)
+        clf = SVC(C=float(C), kernel="precomputed").fit(gtr.entries, train.labels)
+        sk_pred.append(clf.predict(gte.entries))
+        sk_dec.append(clf.decision_function(gte.entries))
+    np.savez_compressed(
+        OUT / "svc_config1.npz", X_train=X_tr, X_test=X_te, y_train=train.labels, y_test=test.labels,
+        K_train=gtr.entries, K_test=gte.entries, C_grid=grid, ref_auc=np.array(ref_auc),
+        ref_accuracy=np.array(ref_acc), sklearn_pred=np.array(sk_pred), sklearn_decision=np.array(sk_dec),
+    )
+    print("svc_config1: best ref AUC", max(ref_auc))
+
+
+def wire_format():
+    """serialize_state bytes of two reference states (mps.py:294-314)."""
+    cfg = ansatz.FeatureMapConfig(6, 2, 2, 0.5)
+    X = np.random.default_rng(8).uniform(0.0, 2.0, (2, 6))
+    states = kernel.simulate_dataset(X, cfg)
+    blobs = [np.frombuffer(mps.serialize_state(s), dtype=np.uint8) for s in states]
+    np.savez_compressed(OUT / "wire_mps1.npz", X=X, blob0=blobs[0], blob1=blobs[1])
+    print("wire_mps1")
+
+
+if __name__ == "__main__" and "--extra" in sys.argv:
+    svc_experiment()
+    wire_format()

@@ -277,3 +277,42 @@ def test_chi_capacity_escalation():
     assert b.chi_cap == 16
     with pytest.raises(RuntimeError):
         simulate_rows(g["X"][:4], cfg, budget, chi_cap=4)
+
+
+def test_wire_format_of_gpu_states():
+    import paper_2411_09336_b200 as P
+
+    g = golden("wire_mps1.npz")
+    ref = [P.deserialize_state(g[k].tobytes()) for k in ("blob0", "blob1")]
+    batch = P.simulate_dataset(g["X"], P.FeatureMapConfig(6, 2, 2, 0.5))
+    for i, r in enumerate(ref):
+        st = P.deserialize_state(P.serialize_state(batch[i]))
+        assert st.bond_dims() == r.bond_dims()
+        assert (st.m, st.ortho_center, st.peak_chi, st.gate_count_1q, st.gate_count_2q) == (
+            r.m, r.ortho_center, r.peak_chi, r.gate_count_1q, r.gate_count_2q)
+        assert abs(abs(np.vdot(P.to_statevector(st), P.to_statevector(r))) - 1) < 1e-12
+
+
+def test_downstream_svc_matches_reference_kernel():
+    """Config 1's experiment flow: blobs -> split -> rescale -> GPU train/test
+    kernels -> SVC over the C grid.  The precomputed-kernel SVC on the GPU K
+    reproduces the predictions made on the reference K (golden), i.e. the same
+    downstream accuracy."""
+    from sklearn.svm import SVC
+
+    import paper_2411_09336_b200 as P
+
+    g = golden("svc_config1.npz")
+    cfg = P.FeatureMapConfig(8, 2, 1, 0.5)
+    ntr, nte = len(g["X_train"]), len(g["X_test"])
+    Ktr = P.run_distributed(g["X_train"], g["X_train"], cfg, P.make_schedule(ntr, ntr, 1, "round_robin", "train"),
+                            budget=0.0).entries
+    Kte = P.run_distributed(g["X_test"], g["X_train"], cfg, P.make_schedule(nte, ntr, 1, "round_robin", "test"),
+                            budget=0.0).entries
+    assert np.abs(Ktr - g["K_train"]).max() < 1e-10 and np.abs(Kte - g["K_test"]).max() < 1e-10
+    for c, pred, dec in zip(g["C_grid"], g["sklearn_pred"], g["sklearn_decision"]):
+        clf = SVC(C=float(c), kernel="precomputed").fit(Ktr, g["y_train"])
+        assert np.array_equal(clf.predict(Kte), pred)
+        assert np.abs(clf.decision_function(Kte) - dec).max() < 1e-6
+    acc = max(np.mean(p == g["y_test"]) for p in g["sklearn_pred"])
+    assert acc >= max(g["ref_accuracy"]) - 1e-12 or acc >= 0.95

@@ -219,3 +219,17 @@ def test_gpu_entry_points_fail_loudly_without_cuda():
         pytest.skip("CUDA present")
     with pytest.raises(RuntimeError, match="CUDA"):
         P.simulate_dataset(np.ones((2, 4)), P.FeatureMapConfig(4, 1, 1, 0.5))
+
+
+def test_mps1_wire_format_round_trip_is_byte_exact():
+    """serialize/deserialize (mps.py:294-340) on the reference's own bytes."""
+    import paper_2411_09336_b200 as P
+
+    g = golden("wire_mps1.npz")
+    for key in ("blob0", "blob1"):
+        blob = g[key].tobytes()
+        st = P.deserialize_state(blob)
+        assert P.serialize_state(st) == blob
+        assert st.m == 6 and st.ortho_center is not None
+    with pytest.raises(ValueError, match="serialized"):
+        P.deserialize_state(b"XXXX" + bytes(40))
