@@ -14,8 +14,8 @@ int fail(int status, const char* fmt, ...);
 int cuda_fail(int err, const char* what);  // err is a cudaError_t
 
 // chi capacities with a compiled simulation + overlap path
-constexpr int kChiCaps[] = {4, 8, 16, 32};
-constexpr int kNumChiCaps = 4;
+constexpr int kChiCaps[] = {4, 8, 16, 32, 48};
+constexpr int kNumChiCaps = 5;
 inline bool chi_cap_supported(int c) {
   for (int x : kChiCaps)
     if (x == c) return true;
@@ -44,6 +44,7 @@ struct SimArgs {
   int32_t* peak;
   int32_t* status;
   int64_t* entry_log;
+  void* scratch;  // set by the launcher (rotation logs of capacities > 32)
 };
 int launch_simulate(const SimArgs& a, void* stream);
 
@@ -57,6 +58,7 @@ struct SvdArgs {
   int32_t* keep;
   double* discarded;
   int32_t* status;
+  void* scratch;
 };
 int launch_svd(const SvdArgs& a, void* stream);
 

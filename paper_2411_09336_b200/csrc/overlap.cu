@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
 // --------------------------------------------------------------- generic chi
 template <int CAP>
 struct O2Cfg {
-  static constexpr int warps = CAP <= 8 ? 8 : CAP <= 16 ? 4 : 2;
+  static constexpr int warps = CAP <= 8 ? 8 : CAP <= 16 ? 4 : CAP <= 32 ? 2 : 1;
   static constexpr int nt = warps * 32;
   static size_t smem() {
     return sizeof(double2) * (2 * CAP * CAP + warps * (CAP * CAP + 2 * CAP * CAP));
@@ -531,6 +531,7 @@ int launch_overlap(const OverlapArgs& a, void* stream) {
     case 8: s = launch_o2<8>(a, st); break;
     case 16: s = launch_o2<16>(a, st); break;
     case 32: s = launch_o2<32>(a, st); break;
+    case 48: s = launch_o2<48>(a, st); break;
     default: return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", a.chi_cap);
   }
   if (s != MPSKQ_OK) return s;
@@ -548,7 +549,8 @@ void tile_shape(int chi_cap, int* rb, int* cb) {
     case 4: *rb = kWarpsO1; *cb = kLanes; return;
     case 8: *rb = 1; *cb = O2Cfg<8>::warps; return;
     case 16: *rb = 1; *cb = O2Cfg<16>::warps; return;
-    default: *rb = 1; *cb = O2Cfg<32>::warps; return;
+    case 32: *rb = 1; *cb = O2Cfg<32>::warps; return;
+    default: *rb = 1; *cb = O2Cfg<48>::warps; return;
   }
 }
 

@@ -332,7 +332,7 @@ int mpskq_simulate(int m, int chi_cap, const int32_t* ops_dev, int64_t n_ops, in
   if (n_states == 0) return MPSKQ_OK;
   SimArgs a{m,        chi_cap,  ops_dev,      n_ops,        n_gates,   coef_dev,
             n_params, n_states, budget,       chi_max,      site_off_dev, state_stride,
-            sites_dev, chi_dev, discard_dev,  peak_chi_dev, status_dev, entry_log_dev};
+            sites_dev, chi_dev, discard_dev,  peak_chi_dev, status_dev, entry_log_dev, nullptr};
   return launch_simulate(a, stream);
 }
 
@@ -349,7 +349,7 @@ int mpskq_svd_truncated_batched(int rows, int cols, int64_t batch, const double*
                 cols, maxdim, maxdim);
   if (batch <= 0) return MPSKQ_OK;
   SvdArgs a{rows, cols, batch, mats_dev, budget, chi_max, u_dev, s_dev, vh_dev, keep_dev,
-            discarded_dev, status_dev};
+            discarded_dev, status_dev, nullptr};
   return launch_svd(a, stream);
 }
 

@@ -34,7 +34,16 @@ constexpr int kMaxSweeps = 40;
 
 template <int CAP>
 struct NtFor {
-  static constexpr int value = CAP <= 4 ? 32 : CAP <= 8 ? 64 : CAP <= 16 ? 128 : 256;
+  static constexpr int value = CAP <= 4 ? 32 : CAP <= 8 ? 64 : CAP <= 16 ? 128 : CAP <= 32 ? 256 : 384;
+};
+
+// Capacities above 32 keep only theta/C in shared memory: the Jacobi rotations
+// are logged to a per-CTA global buffer and replayed on the identity after
+// the C-side factor has been written out (W then reuses C's space).
+template <int CAP>
+struct LogW {
+  static constexpr bool value = CAP > 32;
+  static constexpr int64_t entries = (int64_t)kMaxSweeps * (2 * CAP) * CAP;  // sweeps x rounds x pairs
 };
 
 // shared-memory carve-out of one CTA
@@ -52,9 +61,10 @@ struct Smem {
   int* perm;     // LD
   int* ibuf;     // 4: keep
   int* chi;      // m + 1
+  double4* rlog;  // per-CTA rotation log (capacities > 32 only)
 
   static size_t bytes(int m) {
-    size_t b = sizeof(double2) * (2 * LD * LD + 2 * CAP * CAP + LD);
+    size_t b = sizeof(double2) * ((LogW<CAP>::value ? 1 : 2) * LD * LD + 2 * CAP * CAP + LD);
     b += sizeof(double) * (2 * LD + 32 + 4);
     b += sizeof(int) * (LD + 4 + m + 1);
     return (b + 15) & ~size_t(15);
@@ -63,9 +73,12 @@ struct Smem {
     char* p = static_cast<char*>(base);
     A = reinterpret_cast<double2*>(p);
     p += sizeof(double2) * LD * LD;
-    W = reinterpret_cast<double2*>(p);
-    p += sizeof(double2) * LD * LD;
+    if constexpr (!LogW<CAP>::value) {
+      W = reinterpret_cast<double2*>(p);
+      p += sizeof(double2) * LD * LD;
+    }
     S = reinterpret_cast<double2*>(p);
+    if constexpr (LogW<CAP>::value) W = S;  // Q of a QR move (Rr x k <= 2CAP x CAP)
     p += sizeof(double2) * 2 * CAP * CAP;
     rd = reinterpret_cast<double2*>(p);
     p += sizeof(double2) * LD;
@@ -82,6 +95,7 @@ struct Smem {
     ibuf = reinterpret_cast<int*>(p);
     p += sizeof(int) * 4;
     chi = reinterpret_cast<int*>(p);
+    rlog = nullptr;
     (void)m;
   }
 };
@@ -182,7 +196,8 @@ __device__ __forceinline__ double gsum(double v) {
 }
 
 template <int CAP, int NT, int G>
-__device__ __noinline__ void jacobi_sweeps(Smem<CAP, NT>& sm, int Rr, int n) {
+__device__ __noinline__ int jacobi_sweeps(Smem<CAP, NT>& sm, int Rr, int n) {
+  constexpr bool kLog = LogW<CAP>::value;
   constexpr int LD = 2 * CAP;
   const int tid = threadIdx.x;
   double2* A = sm.A;
@@ -192,7 +207,8 @@ __device__ __noinline__ void jacobi_sweeps(Smem<CAP, NT>& sm, int Rr, int n) {
   // convergence: |c_p^H c_q| <= tol * |c_p| |c_q|, compared in squares
   const double tol = DBL_EPSILON * (double)max(Rr, 8);
   const double tol2 = tol * tol;
-  for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
+  int sweep = 0;
+  while (sweep < kMaxSweeps) {
     int rotated = 0;
     for (int t = 0; t < span; ++t) {
       // circle method: position 0 is fixed, positions 1..ne-1 rotate by t
@@ -227,7 +243,11 @@ __device__ __noinline__ void jacobi_sweeps(Smem<CAP, NT>& sm, int Rr, int n) {
       gx = gsum<G>(gx);
       gy = gsum<G>(gy);
       const double g2 = fma(gx, gx, gy * gy);
-      if (act && g2 > tol2 * a * b && g2 > 0.0) {
+      const bool rot = act && g2 > tol2 * a * b && g2 > 0.0;
+      double4* entry = nullptr;
+      if constexpr (kLog) entry = sm.rlog + ((int64_t)sweep * span + t) * P + k;
+      if (kLog && act && g == 0 && !rot) *entry = make_double4(1.0, 0.0, 0.0, 0.0);
+      if (rot) {
         rotated = 1;
         const double inv = rsqrt(g2);  // 1/|gamma|
         const double zeta = (b - a) * (0.5 * inv);
@@ -244,39 +264,102 @@ __device__ __noinline__ void jacobi_sweeps(Smem<CAP, NT>& sm, int Rr, int n) {
           A[p * LD + r] = csub(cscale(x, c), cmul(cconj(se), y));
           A[q * LD + r] = cadd(cmul(se, x), cscale(y, c));
         }
-        #pragma unroll 1
-        for (int r = g; r < n; r += G) {
-          const double2 x = W[p * LD + r], y = W[q * LD + r];
-          W[p * LD + r] = csub(cscale(x, c), cmul(cconj(se), y));
-          W[q * LD + r] = cadd(cmul(se, x), cscale(y, c));
+        if constexpr (kLog) {
+          if (g == 0) *entry = make_double4(c, se.x, se.y, 1.0);
+        } else {
+          #pragma unroll 1
+          for (int r = g; r < n; r += G) {
+            const double2 x = W[p * LD + r], y = W[q * LD + r];
+            W[p * LD + r] = csub(cscale(x, c), cmul(cconj(se), y));
+            W[q * LD + r] = cadd(cmul(se, x), cscale(y, c));
+          }
         }
       }
       bsync<NT>();
     }
+    ++sweep;
     if (!block_any<NT>(rotated)) break;
+  }
+  return sweep;
+}
+
+// Log mode: W = I_n in `Wm`, then apply the logged rotations in order.
+template <int CAP, int NT, int G>
+__device__ __noinline__ void replay_sweeps(Smem<CAP, NT>& sm, double2* Wm, int n, int sweeps) {
+  constexpr int LD = 2 * CAP;
+  const int tid = threadIdx.x;
+  const int ne = n + (n & 1), P = ne >> 1, span = ne - 1;
+  const int k = tid / G, g = tid % G;
+  for (int sweep = 0; sweep < sweeps; ++sweep) {
+    for (int t = 0; t < span; ++t) {
+      int p = 0, q = 0;
+      if (k < P) {
+        const int pa = k, pb = ne - 1 - k;
+        int x = pa - 1 + t, y = pb - 1 + t;
+        x = x >= span ? x - span : x;
+        y = y >= span ? y - span : y;
+        p = pa == 0 ? 0 : 1 + x;
+        q = 1 + y;
+        if (p > q) {
+          const int tmp = p;
+          p = q;
+          q = tmp;
+        }
+      }
+      if (k < P && q < n) {
+        const double4 e = sm.rlog[((int64_t)sweep * span + t) * P + k];
+        if (e.w != 0.0) {
+          const double c = e.x;
+          const double2 se = make_double2(e.y, e.z);
+          #pragma unroll 1
+          for (int r = g; r < n; r += G) {
+            const double2 x = Wm[p * LD + r], y = Wm[q * LD + r];
+            Wm[p * LD + r] = csub(cscale(x, c), cmul(cconj(se), y));
+            Wm[q * LD + r] = cadd(cmul(se, x), cscale(y, c));
+          }
+        }
+      }
+      bsync<NT>();
+    }
   }
 }
 
 template <int CAP, int NT>
-__device__ void jacobi(Smem<CAP, NT>& sm, int Rr, int n) {
+__device__ void init_identity(double2* Wm, int n) {
   constexpr int LD = 2 * CAP;
-  const int tid = threadIdx.x;
   #pragma unroll 1
-  for (int idx = tid; idx < n * n; idx += NT) {
+  for (int idx = threadIdx.x; idx < n * n; idx += NT) {
     const int c = idx / n, r = idx - c * n;
-    sm.W[c * LD + r] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+    Wm[c * LD + r] = make_double2(r == c ? 1.0 : 0.0, 0.0);
   }
   bsync<NT>();
-  if (n < 2) return;
+}
+
+// returns the number of sweeps run (needed by the log-mode replay)
+template <int CAP, int NT>
+__device__ int jacobi(Smem<CAP, NT>& sm, int Rr, int n) {
+  if constexpr (!LogW<CAP>::value) init_identity<CAP, NT>(sm.W, n);
+  if (n < 2) return 0;
   // lanes per column pair: G * (n/2) <= NT, G in {8, 16, 32} for every
   // (CAP, NT) instantiation (NT >= 8 * CAP)
   const int G = group_width<NT>((n + 1) >> 1);
+  if (G >= 32) return jacobi_sweeps<CAP, NT, 32>(sm, Rr, n);
+  if (G == 16) return jacobi_sweeps<CAP, NT, 16>(sm, Rr, n);
+  return jacobi_sweeps<CAP, NT, 8>(sm, Rr, n);
+}
+
+// log mode: rebuild W (n x n) in Wm from the rotation log
+template <int CAP, int NT>
+__device__ void replay(Smem<CAP, NT>& sm, double2* Wm, int n, int sweeps) {
+  init_identity<CAP, NT>(Wm, n);
+  if (n < 2) return;
+  const int G = group_width<NT>((n + 1) >> 1);
   if (G >= 32)
-    jacobi_sweeps<CAP, NT, 32>(sm, Rr, n);
+    replay_sweeps<CAP, NT, 32>(sm, Wm, n, sweeps);
   else if (G == 16)
-    jacobi_sweeps<CAP, NT, 16>(sm, Rr, n);
+    replay_sweeps<CAP, NT, 16>(sm, Wm, n, sweeps);
   else
-    jacobi_sweeps<CAP, NT, 8>(sm, Rr, n);
+    replay_sweeps<CAP, NT, 8>(sm, Wm, n, sweeps);
 }
 
 // column norms of C, descending order in perm (ties keep index order)
@@ -397,9 +480,6 @@ __device__ void op_qr_left(Smem<CAP, NT>& sm, StateCtx& st, int i) {
     const int r = idx / chr, c = idx - r * chr;
     sm.A[c * LD + r] = M[idx];
   }
-  const int nn = chr * 2 * chn;
-  #pragma unroll 1
-  for (int idx = tid; idx < nn; idx += NT) sm.S[idx] = N[idx];
   bsync<NT>();
   const int k = householder_qr<CAP, NT>(sm, Rr, chr);
   #pragma unroll 1
@@ -407,6 +487,11 @@ __device__ void op_qr_left(Smem<CAP, NT>& sm, StateCtx& st, int i) {
     const int r = idx / k, c = idx - r * k;
     M[idx] = sm.W[c * LD + r];
   }
+  bsync<NT>();  // Q is out: W may alias S (capacities > 32)
+  const int nn = chr * 2 * chn;
+  #pragma unroll 1
+  for (int idx = tid; idx < nn; idx += NT) sm.S[idx] = N[idx];
+  bsync<NT>();
   const int cols = 2 * chn;
   #pragma unroll 1
   for (int idx = tid; idx < k * cols; idx += NT) {
@@ -434,9 +519,6 @@ __device__ void op_qr_right(Smem<CAP, NT>& sm, StateCtx& st, int i) {
     const int c = idx / Rr, r = idx - c * Rr;
     sm.A[c * LD + r] = cconj(M[idx]);
   }
-  const int np = 2 * chp * chl;
-  #pragma unroll 1
-  for (int idx = tid; idx < np; idx += NT) sm.S[idx] = P[idx];
   bsync<NT>();
   const int k = householder_qr<CAP, NT>(sm, Rr, chl);
   #pragma unroll 1
@@ -444,6 +526,11 @@ __device__ void op_qr_right(Smem<CAP, NT>& sm, StateCtx& st, int i) {
     const int kk = idx / Rr, r = idx - kk * Rr;
     M[idx] = cconj(sm.W[kk * LD + r]);
   }
+  bsync<NT>();  // Q is out: W may alias S (capacities > 32)
+  const int np = 2 * chp * chl;
+  #pragma unroll 1
+  for (int idx = tid; idx < np; idx += NT) sm.S[idx] = P[idx];
+  bsync<NT>();
   const int rows = 2 * chp;
   #pragma unroll 1
   for (int idx = tid; idx < rows * k; idx += NT) {
@@ -467,13 +554,20 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
   double2* X = st.base + st.off[q];
   double2* Y = st.base + st.off[q + 1];
   const int Mr = 2 * chl, Nc = 2 * chr;
-  double2* Xs = sm.W;
-  double2* Ys = sm.W + 2 * CAP * CAP;
-  #pragma unroll 1
-  for (int idx = tid; idx < Mr * chm; idx += NT) Xs[idx] = X[idx];
-  #pragma unroll 1
-  for (int idx = tid; idx < chm * Nc; idx += NT) Ys[idx] = Y[idx];
-  bsync<NT>();
+  constexpr bool kLog = LogW<CAP>::value;
+  const double2* Xs = X;  // capacities > 32 read the sites straight from L1/L2
+  const double2* Ys = Y;
+  if constexpr (!kLog) {
+    double2* xs = sm.W;
+    double2* ys = sm.W + 2 * CAP * CAP;
+    #pragma unroll 1
+    for (int idx = tid; idx < Mr * chm; idx += NT) xs[idx] = X[idx];
+    #pragma unroll 1
+    for (int idx = tid; idx < chm * Nc; idx += NT) ys[idx] = Y[idx];
+    bsync<NT>();
+    Xs = xs;
+    Ys = ys;
+  }
   // theta = site_q . site_{q+1} (mps.py:183), gate on the physical legs
   // (:184-186); every item produces the two entries the gate couples.
   const double c = cs.x, s = cs.y;
@@ -520,7 +614,7 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
   const int Rr = left ? Mr : Nc;
   const int n = left ? Nc : Mr;
   const int kmin = min(Mr, Nc);
-  jacobi<CAP, NT>(sm, Rr, n);
+  const int sweeps = jacobi<CAP, NT>(sm, Rr, n);
   norms_and_order<CAP, NT>(sm, Rr, n);
   if (tid == 0) truncation_rule<CAP, NT>(sm, kmin, budget, chi_max);
   bsync<NT>();
@@ -530,29 +624,41 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
     st.status = MPSKQ_STATE_CAPACITY;
     return;
   }
+  // C side first (it lives in A), then W (log mode rebuilds it in A)
   if (left) {
-    // site_q = U s (mps.py:194), site_{q+1} = Vh
+    // site_q = U s (mps.py:194)
     #pragma unroll 1
     for (int idx = tid; idx < Mr * keep; idx += NT) {
       const int row = idx / keep, kk = idx - row * keep;
       X[idx] = cscale(sm.A[sm.perm[kk] * LD + row], factor);
     }
-    #pragma unroll 1
-    for (int idx = tid; idx < keep * Nc; idx += NT) {
-      const int kk = idx / Nc, col = idx - kk * Nc;
-      Y[idx] = cconj(sm.W[sm.perm[kk] * LD + col]);
-    }
   } else {
-    // site_q = U, site_{q+1} = s Vh (mps.py:197-199)
-    #pragma unroll 1
-    for (int idx = tid; idx < Mr * keep; idx += NT) {
-      const int row = idx / keep, kk = idx - row * keep;
-      X[idx] = sm.W[sm.perm[kk] * LD + row];
-    }
+    // site_{q+1} = s Vh (mps.py:197-199)
     #pragma unroll 1
     for (int idx = tid; idx < keep * Nc; idx += NT) {
       const int kk = idx / Nc, col = idx - kk * Nc;
       Y[idx] = cscale(cconj(sm.A[sm.perm[kk] * LD + col]), factor);
+    }
+  }
+  const double2* Wm = sm.W;
+  if constexpr (kLog) {
+    bsync<NT>();
+    replay<CAP, NT>(sm, sm.A, n, sweeps);
+    Wm = sm.A;
+  }
+  if (left) {
+    // site_{q+1} = Vh
+    #pragma unroll 1
+    for (int idx = tid; idx < keep * Nc; idx += NT) {
+      const int kk = idx / Nc, col = idx - kk * Nc;
+      Y[idx] = cconj(Wm[sm.perm[kk] * LD + col]);
+    }
+  } else {
+    // site_q = U
+    #pragma unroll 1
+    for (int idx = tid; idx < Mr * keep; idx += NT) {
+      const int row = idx / keep, kk = idx - row * keep;
+      X[idx] = Wm[sm.perm[kk] * LD + row];
     }
   }
   if (tid == 0) {
@@ -570,6 +676,8 @@ __global__ void __launch_bounds__(NT) sim_kernel(SimArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<CAP, NT> sm;
   sm.carve(smem_raw, a.m);
+  if constexpr (LogW<CAP>::value)
+    sm.rlog = static_cast<double4*>(a.scratch) + (int64_t)blockIdx.x * LogW<CAP>::entries;
   const int tid = threadIdx.x;
   const int m = a.m;
   const int4* ops = reinterpret_cast<const int4*>(a.ops);
@@ -632,6 +740,8 @@ __global__ void __launch_bounds__(NT) svd_kernel(SvdArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<CAP, NT> sm;
   sm.carve(smem_raw, 0);
+  if constexpr (LogW<CAP>::value)
+    sm.rlog = static_cast<double4*>(a.scratch) + (int64_t)blockIdx.x * LogW<CAP>::entries;
   const int tid = threadIdx.x;
   const int rows = a.rows, cols = a.cols, kmin = min(rows, cols);
   for (int64_t b = blockIdx.x; b < a.batch; b += gridDim.x) {
@@ -648,7 +758,7 @@ __global__ void __launch_bounds__(NT) svd_kernel(SvdArgs a) {
       if (tid == 0) a.status[b] = MPSKQ_STATE_NONFINITE;
       continue;
     }
-    jacobi<CAP, NT>(sm, rows, cols);
+    const int sweeps = jacobi<CAP, NT>(sm, rows, cols);
     norms_and_order<CAP, NT>(sm, rows, cols);
     if (tid == 0) truncation_rule<CAP, NT>(sm, kmin, a.budget, a.chi_max);
     bsync<NT>();
@@ -667,10 +777,16 @@ __global__ void __launch_bounds__(NT) svd_kernel(SvdArgs a) {
       U[idx] = nrm > 0.0 ? cscale(sm.A[sm.perm[k] * LD + r], 1.0 / nrm) : cz();
     }
     double2* Vh = reinterpret_cast<double2*>(a.vh) + b * kmin * cols;
+    const double2* Wm = sm.W;
+    if constexpr (LogW<CAP>::value) {
+      bsync<NT>();
+      replay<CAP, NT>(sm, sm.A, cols, sweeps);
+      Wm = sm.A;
+    }
     #pragma unroll 1
     for (int idx = tid; idx < kmin * cols; idx += NT) {
       const int k = idx / cols, c = idx - k * cols;
-      Vh[idx] = cconj(sm.W[sm.perm[k] * LD + c]);
+      Vh[idx] = cconj(Wm[sm.perm[k] * LD + c]);
     }
     if (tid == 0) {
       a.keep[b] = sm.ibuf[0];
@@ -693,26 +809,48 @@ int prepare(K kernel, size_t smem) {
   return MPSKQ_OK;
 }
 
+// grid and rotation-log scratch; capacities > 32 run one persistent CTA per SM
 template <int CAP>
-int launch_sim_cap(const SimArgs& a, cudaStream_t st) {
+int plan_grid(int64_t items, cudaStream_t st, int64_t* grid, void** scratch) {
+  *grid = items < (int64_t(1) << 30) ? items : (int64_t(1) << 30);
+  *scratch = nullptr;
+  if constexpr (LogW<CAP>::value) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    *grid = items < sms ? items : sms;
+    cudaError_t e = cudaMallocAsync(scratch, sizeof(double4) * LogW<CAP>::entries * *grid, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(rotation log)");
+  }
+  return MPSKQ_OK;
+}
+
+template <int CAP>
+int launch_sim_cap(const SimArgs& a0, cudaStream_t st) {
   constexpr int NT = NtFor<CAP>::value;
-  const size_t smem = Smem<CAP, NT>::bytes(a.m);
+  const size_t smem = Smem<CAP, NT>::bytes(a0.m);
   if (int s = prepare(sim_kernel<CAP, NT>, smem)) return s;
-  const int64_t grid = a.n_states < (int64_t(1) << 30) ? a.n_states : (int64_t(1) << 30);
+  SimArgs a = a0;
+  int64_t grid = 0;
+  if (int s = plan_grid<CAP>(a.n_states, st, &grid, &a.scratch)) return s;
   sim_kernel<CAP, NT><<<(unsigned)grid, NT, smem, st>>>(a);
   cudaError_t e = cudaGetLastError();
+  if (a.scratch) cudaFreeAsync(a.scratch, st);
   if (e != cudaSuccess) return cuda_fail(e, "sim_kernel launch");
   return MPSKQ_OK;
 }
 
 template <int CAP>
-int launch_svd_cap(const SvdArgs& a, cudaStream_t st) {
+int launch_svd_cap(const SvdArgs& a0, cudaStream_t st) {
   constexpr int NT = NtFor<CAP>::value;
   const size_t smem = Smem<CAP, NT>::bytes(0);
   if (int s = prepare(svd_kernel<CAP, NT>, smem)) return s;
-  const int64_t grid = a.batch < (int64_t(1) << 30) ? a.batch : (int64_t(1) << 30);
+  SvdArgs a = a0;
+  int64_t grid = 0;
+  if (int s = plan_grid<CAP>(a.batch, st, &grid, &a.scratch)) return s;
   svd_kernel<CAP, NT><<<(unsigned)grid, NT, smem, st>>>(a);
   cudaError_t e = cudaGetLastError();
+  if (a.scratch) cudaFreeAsync(a.scratch, st);
   if (e != cudaSuccess) return cuda_fail(e, "svd_kernel launch");
   return MPSKQ_OK;
 }
@@ -726,6 +864,7 @@ int launch_simulate(const SimArgs& a, void* stream) {
     case 8: return launch_sim_cap<8>(a, st);
     case 16: return launch_sim_cap<16>(a, st);
     case 32: return launch_sim_cap<32>(a, st);
+    case 48: return launch_sim_cap<48>(a, st);
   }
   return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", a.chi_cap);
 }
@@ -736,7 +875,8 @@ int launch_svd(const SvdArgs& a, void* stream) {
   if (big <= 8) return launch_svd_cap<4>(a, st);
   if (big <= 16) return launch_svd_cap<8>(a, st);
   if (big <= 32) return launch_svd_cap<16>(a, st);
-  return launch_svd_cap<32>(a, st);
+  if (big <= 64) return launch_svd_cap<32>(a, st);
+  return launch_svd_cap<48>(a, st);
 }
 
 // FP64 FMA throughput probe: 16 independent DFMA chains per thread

@@ -365,7 +365,8 @@ def simulate_program(prog: Program, coef, budget: float, chi_max: int = 0,
             raise ValueError("tensor has non-finite entries")
         if np.any(st == N.STATE_CAPACITY):
             continue
-        _CAP_HINT[key] = cap
+        if chi_cap is None:
+            _CAP_HINT[key] = cap
         return MpsBatch(m, cap, off, stride, sites, chi, disc, peak, budget, prog.gate_count_1q,
                         prog.gate_count_2q, prog.final_center, elog, tm.seconds())
     raise RuntimeError(f"bond dimension exceeds the largest usable chi capacity {order[-1]}")

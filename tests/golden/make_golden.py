@@ -192,7 +192,7 @@ def acceptance_c1():
     print("acceptance_c1:", len(cases))
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     OUT.mkdir(parents=True, exist_ok=True)
     svd_cases()
     schedule_cases()
@@ -254,3 +254,33 @@ def wire_format():
 if __name__ == "__main__" and "--extra" in sys.argv:
     svc_experiment()
     wire_format()
+
+
+if __name__ == "__main__" and "--large-chi" in sys.argv:
+    # config 5 (interaction-distance sweep at m=100, budget 1e-16): d=6 and d=8
+    # need chi > 32, i.e. the capacity-48 path
+    gram_case("config5_m100_d6", 100, 2, 6, 0.1, 1e-16, 4, 2, seed=0)
+    gram_case("config5_m100_d8", 100, 2, 8, 0.1, 1e-16, 4, 2, seed=0)
+
+
+def svd_cases_large():
+    """svd_truncated on 65..96-sized matrices (the capacity-48 device path)."""
+    rng = np.random.default_rng(77)
+    out = {}
+    for idx, (rows, cols, budget) in enumerate([(80, 80, 1e-16), (96, 90, 1e-24), (70, 96, 1e-20)]):
+        k = min(rows, cols)
+        q1, _ = np.linalg.qr(rng.normal(size=(rows, rows)) + 1j * rng.normal(size=(rows, rows)))
+        q2, _ = np.linalg.qr(rng.normal(size=(cols, cols)) + 1j * rng.normal(size=(cols, cols)))
+        sv = np.geomspace(1.0, 1e-14, k)
+        mat = (q1[:, :k] * sv) @ q2[:k, :]
+        res = tensor.svd_truncated(mat, 1, budget)
+        out[f"mat{idx}"] = mat
+        out[f"budget{idx}"] = budget
+        out[f"s{idx}"] = res.singular_values
+        out[f"disc{idx}"] = res.discarded_weight
+    np.savez_compressed(OUT / "svd_cases_large.npz", **out)
+    print("svd_cases_large")
+
+
+if __name__ == "__main__" and "--svd-large" in sys.argv:
+    svd_cases_large()

@@ -316,3 +316,52 @@ def test_downstream_svc_matches_reference_kernel():
         assert np.abs(clf.decision_function(Kte) - dec).max() < 1e-6
     acc = max(np.mean(p == g["y_test"]) for p in g["sklearn_pred"])
     assert acc >= max(g["ref_accuracy"]) - 1e-12 or acc >= 0.95
+
+
+def test_capacity_48_path_matches_reference():
+    """chi capacity 48 (theta up to 96x96): Jacobi rotations logged and replayed.
+    Config 5 at d=6 (m=100, budget 1e-16) needs it: final bonds reach 31 but
+    the running peak_chi reaches 36 (mps.py:202)."""
+    import paper_2411_09336_b200 as P
+    from paper_2411_09336_b200.kernel import simulate_rows
+
+    g = golden("config5_m100_d6.npz")
+    cfg, budget = _cfg(g)
+    b = simulate_rows(g["X"], cfg, budget, chi_cap=48)
+    assert b.chi_cap == 48
+    assert np.array_equal(b.bond_dims(), g["train_chi"])
+    K = P.compute_gram(b, b, "train").entries
+    assert np.abs(K - g["K_train"]).max() < 1e-6
+    assert np.array_equal(b.peak.cpu().numpy(), g["train_peak"])
+    # the automatic capacity choice escalates past 32 by itself
+    auto = P.simulate_dataset(g["X"], cfg, budget=budget)
+    assert auto.chi_cap == 48 and np.array_equal(auto.bond_dims(), g["train_chi"])
+    with pytest.raises(RuntimeError):
+        simulate_rows(g["X"], cfg, budget, chi_cap=32)
+
+
+def test_capacity_overflow_is_reported():
+    """config 5 at d=8 reaches chi 59 on these rows: beyond the largest
+    compiled capacity (48) the engine raises instead of truncating silently."""
+    import paper_2411_09336_b200 as P
+
+    g = golden("config5_m100_d8.npz")
+    cfg, budget = _cfg(g)
+    with pytest.raises(RuntimeError, match="capacity"):
+        P.simulate_dataset(g["X"][:1], cfg, budget=budget)
+
+
+def test_svd_truncated_large_matrices():
+    import paper_2411_09336_b200 as P
+
+    g = golden("svd_cases_large.npz")
+    for i in range(3):
+        A = g[f"mat{i}"]
+        res = P.svd_truncated(A, 1, float(g[f"budget{i}"]))
+        s = g[f"s{i}"]
+        assert res.singular_values.size == s.size
+        assert np.abs(res.singular_values - s).max() < 1e-13
+        U, Vh = res.left, res.right
+        k = s.size
+        assert np.abs(U.conj().T @ U - np.eye(k)).max() < 1e-11
+        assert np.abs(Vh @ Vh.conj().T - np.eye(k)).max() < 1e-11
