@@ -209,13 +209,22 @@ def gpu_main(args) -> None:
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_sample(n, args.cpu_seconds)  # before CUDA init (forked workers)
 
+    # MPSKQ_BENCH_SHARE_GPU=1 maps every rank onto cuda:0 and uses gloo (host
+    # collectives): a functional check of the multi-rank path on a 1-GPU box.
+    # The ranks' kernels never wait on each other.  Real runs use NCCL.
+    share = os.environ.get("MPSKQ_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2411_09336_b200 as P
     from paper_2411_09336_b200 import _native as N
     from paper_2411_09336_b200.ansatz import feature_map_topology
-    from paper_2411_09336_b200.distributed import shard
+    from paper_2411_09336_b200.distributed import _all_reduce_max, _reduce_sum_to0, allgather_rows, shard
     from paper_2411_09336_b200.kernel import encode_device, simulate_rows
     from paper_2411_09336_b200.mps import batch_layout, compile_program
 
@@ -233,9 +242,7 @@ def gpu_main(args) -> None:
     # capacity the states need (public path, also warms the library up)
     cap = simulate_rows(X[lo:hi], cfg, BUDGET).chi_cap
     if world > 1:
-        t = torch.tensor([cap], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        cap = int(t.item())
+        cap = int(_all_reduce_max(torch.tensor([cap], device=dev)).item())
     off, stride = batch_layout(M, cap)
     off_d = torch.from_numpy(off).to(dev)
     coef = torch.empty((nloc, prog.n_params, 2), dtype=torch.float64, device=dev)
@@ -247,11 +254,13 @@ def gpu_main(args) -> None:
     status = torch.zeros(nloc, dtype=torch.int32, device=dev)
     counts = [shard(n, world, r)[1] - shard(n, world, r)[0] for r in range(world)]
     mx = max(counts)
-    if world > 1:
+    nccl = world > 1 and dist.get_backend() == "nccl"
+    if nccl:
         pad_sites = torch.zeros((mx, 2 * stride), dtype=torch.float64, device=dev)
         pad_chi = torch.ones((mx, M + 1), dtype=torch.int32, device=dev)
         g_sites = torch.empty((world * mx, 2 * stride), dtype=torch.float64, device=dev)
         g_chi = torch.empty((world * mx, M + 1), dtype=torch.int32, device=dev)
+    if world > 1:
         sites_all = torch.empty((n, 2 * stride), dtype=torch.float64, device=dev)
         chi_all = torch.empty((n, M + 1), dtype=torch.int32, device=dev)
     else:
@@ -268,7 +277,7 @@ def gpu_main(args) -> None:
                                    prog.n_params, nloc, BUDGET, 0, off_d.data_ptr(), stride, sites_loc.data_ptr(),
                                    chi_loc.data_ptr(), disc.data_ptr(), peak.data_ptr(), status.data_ptr(), None, sp))
         e[1].record()
-        if world > 1:  # the one exchange: all-gather of the packed MPS + bond dims
+        if nccl:  # the one exchange: all-gather of the packed MPS + bond dims
             pad_sites[:nloc].copy_(sites_loc)
             pad_chi[:nloc].copy_(chi_loc)
             dist.all_gather_into_tensor(g_sites, pad_sites)
@@ -278,14 +287,20 @@ def gpu_main(args) -> None:
                 sites_all[o : o + c].copy_(g_sites[r * mx : r * mx + c])
                 chi_all[o : o + c].copy_(g_chi[r * mx : r * mx + c])
                 o += c
+        elif world > 1:
+            sites_all.copy_(allgather_rows(sites_loc, counts))
+            chi_all.copy_(allgather_rows(chi_loc, counts))
+        if world > 1:
             K.zero_()
         e[2].record()
         N.check(lib.mpskq_overlap(N.KIND_TRAIN, N.OUT_KERNEL, M, cap, off_d.data_ptr(), stride, sites_all.data_ptr(),
                                   chi_all.data_ptr(), n, sites_all.data_ptr(), chi_all.data_ptr(), n, rank, world,
                                   K.data_ptr(), n, sp))
         e[3].record()
-        if world > 1:
+        if nccl:
             dist.reduce(K, dst=0, op=dist.ReduceOp.SUM)
+        elif world > 1:
+            K.copy_(_reduce_sum_to0(K))
         e[4].record()
 
     for _ in range(args.warmup):
@@ -314,8 +329,7 @@ def gpu_main(args) -> None:
     red_ms = float(np.mean([e[3].elapsed_time(e[4]) for e in ev]))
     if world > 1:
         t = torch.tensor([ms, sim_ms, comm_ms, ov_ms, red_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, sim_ms, comm_ms, ov_ms, red_ms = t.tolist()
+        ms, sim_ms, comm_ms, ov_ms, red_ms = _all_reduce_max(t).tolist()
 
     # parity spot check of this very run against the CPU oracle (rows 0..5)
     spot = None
@@ -368,8 +382,7 @@ def gpu_main(args) -> None:
         torch.cuda.synchronize()
         dist.barrier()
         t = torch.tensor([(time.perf_counter() - w0) / args.steps], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = 1e3 * t.item()
+        e2e_ms = 1e3 * _all_reduce_max(t).item()
         e2e = {"value": n * (n - 1) / 2 / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": X.nbytes,
                "d2h_bytes_per_step": n * n * 8, "ms_per_step": e2e_ms,
                "path": "public API run_distributed (host rows -> host K on rank 0), max over ranks"}
