@@ -204,7 +204,7 @@ def gpu_main(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    n = args.n
+    n = args.rows
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_sample(n, args.cpu_seconds)  # before CUDA init (forked workers)
@@ -455,7 +455,7 @@ def reference_main(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    n = args.n
+    n = args.rows
     seconds = max(2.0, args.ref_seconds)
     for _ in range(args.warmup):
         cpu_sample(n, 0.5)
@@ -498,7 +498,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--n", type=int, default=6400)
+    ap.add_argument("--rows", type=int, default=6400, help="N feature rows (train kernel N x N)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=8.0)
