@@ -529,7 +529,9 @@ int launch_overlap(const OverlapArgs& a, void* stream) {
   switch (a.chi_cap) {
     case 4: s = launch_o1(a, st); break;
     case 8: s = launch_o2<8>(a, st); break;
+    case 12: s = launch_o2<12>(a, st); break;
     case 16: s = launch_o2<16>(a, st); break;
+    case 24: s = launch_o2<24>(a, st); break;
     case 32: s = launch_o2<32>(a, st); break;
     case 48: s = launch_o2<48>(a, st); break;
     default: return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", a.chi_cap);
@@ -548,7 +550,9 @@ void tile_shape(int chi_cap, int* rb, int* cb) {
   switch (chi_cap) {
     case 4: *rb = kWarpsO1; *cb = kLanes; return;
     case 8: *rb = 1; *cb = O2Cfg<8>::warps; return;
+    case 12: *rb = 1; *cb = O2Cfg<12>::warps; return;
     case 16: *rb = 1; *cb = O2Cfg<16>::warps; return;
+    case 24: *rb = 1; *cb = O2Cfg<24>::warps; return;
     case 32: *rb = 1; *cb = O2Cfg<32>::warps; return;
     default: *rb = 1; *cb = O2Cfg<48>::warps; return;
   }

@@ -862,7 +862,9 @@ int launch_simulate(const SimArgs& a, void* stream) {
   switch (a.chi_cap) {
     case 4: return launch_sim_cap<4>(a, st);
     case 8: return launch_sim_cap<8>(a, st);
+    case 12: return launch_sim_cap<12>(a, st);
     case 16: return launch_sim_cap<16>(a, st);
+    case 24: return launch_sim_cap<24>(a, st);
     case 32: return launch_sim_cap<32>(a, st);
     case 48: return launch_sim_cap<48>(a, st);
   }
@@ -874,7 +876,9 @@ int launch_svd(const SvdArgs& a, void* stream) {
   const int big = a.rows > a.cols ? a.rows : a.cols;
   if (big <= 8) return launch_svd_cap<4>(a, st);
   if (big <= 16) return launch_svd_cap<8>(a, st);
+  if (big <= 24) return launch_svd_cap<12>(a, st);
   if (big <= 32) return launch_svd_cap<16>(a, st);
+  if (big <= 48) return launch_svd_cap<24>(a, st);
   if (big <= 64) return launch_svd_cap<32>(a, st);
   return launch_svd_cap<48>(a, st);
 }

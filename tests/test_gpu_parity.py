@@ -274,7 +274,7 @@ def test_chi_capacity_escalation():
     g = golden("config2_m50_d2.npz")
     cfg, budget = _cfg(g)
     b = simulate_rows(g["X"][:4], cfg, budget)
-    assert b.chi_cap == 16
+    assert b.chi_cap == 12
     with pytest.raises(RuntimeError):
         simulate_rows(g["X"][:4], cfg, budget, chi_cap=4)
 
