@@ -179,10 +179,11 @@ __device__ __forceinline__ void o1_phase2_rows(const double2* A, const double2 (
 }
 
 template <int AL>
-__device__ __forceinline__ void o1_phase2_al(const double2* A, const double2 (&T)[kP][2][kP], bool wide,
+__device__ __forceinline__ void o1_phase2_al(const double2* A, const double2 (&T)[kP][2][kP], int na1,
                                              double2 (&env)[kP][kP]) {
   o1_phase2_rows<AL, 0, 2>(A, T, env);
-  if (wide) o1_phase2_rows<AL, 2, 2>(A, T, env);
+  if (na1 > 2) o1_phase2_rows<AL, 2, 1>(A, T, env);
+  if (na1 > 3) o1_phase2_rows<AL, 3, 1>(A, T, env);
 }
 
 __device__ __forceinline__ void o1_phase2(const double2* A, const double2 (&T)[kP][2][kP], int na, int na1,
@@ -191,11 +192,10 @@ __device__ __forceinline__ void o1_phase2(const double2* A, const double2 (&T)[k
   for (int ar = 0; ar < kP; ++ar)
 #pragma unroll
     for (int br = 0; br < kP; ++br) env[ar][br] = make_double2(0.0, 0.0);
-  const bool wide = na1 > 2;
-  o1_phase2_al<0>(A, T, wide, env);
-  if (na > 1) o1_phase2_al<1>(A, T, wide, env);
-  if (na > 2) o1_phase2_al<2>(A, T, wide, env);
-  if (na > 3) o1_phase2_al<3>(A, T, wide, env);
+  o1_phase2_al<0>(A, T, na1, env);
+  if (na > 1) o1_phase2_al<1>(A, T, na1, env);
+  if (na > 2) o1_phase2_al<2>(A, T, na1, env);
+  if (na > 3) o1_phase2_al<3>(A, T, na1, env);
 }
 
 // One CTA = 8 bras (warps) x 32 kets (lanes); one thread owns one pair's 4x4
