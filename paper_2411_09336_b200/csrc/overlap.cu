@@ -16,8 +16,9 @@
 //    divergence and padding costs only up to the block maximum.  Pure FP64
 //    FMA issue; no tensor cores (tcgen05 has no FP64 kind; DMMA only pays
 //    off for dense chi >= 16 contractions).
-//  * generic chi (capacities 8..32): one warp per pair, environments and
-//    intermediates in shared memory, exact bond dims from the batch layout.
+//  * generic chi (capacities 8..48): one warp per pair, both site
+//    contractions as complex GEMM tiles on the FP64 tensor cores (DMMA),
+//    exact bond dims from the batch layout.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -309,17 +310,47 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
   }
 }
 
-// --------------------------------------------------------------- generic chi
+// --------------------------------------------------------------- generic chi (DMMA)
+// One warp per (bra, ket) pair, exact bond dims from the batch layout.  Both
+// halves of the site step are complex GEMMs on FP64 tensor cores
+// (mma.sync.m8n8k4.f64; a complex tile product is 4 real DMMAs):
+//   phase 1  T  (a  x 2b1) = env (a x b) . B (b x 2b1)            B = ket site
+//   phase 2  E' (a1 x b1)  = conj(A)^T (a1 x 2a) . T2 (2a x b1)   T2 = T reshaped
+// env and T live in per-warp shared-memory planes (re / im, zero padded to
+// whole tiles, leading dims = 4 mod 16 so fragment loads are conflict free);
+// the site tensors are read straight from global memory into fragments (the
+// bra is shared by the CTA's warps through L1).  Warps never synchronise with
+// each other.
 template <int CAP>
-struct O2Cfg {
-  static constexpr int warps = CAP <= 8 ? 8 : CAP <= 16 ? 4 : CAP <= 32 ? 2 : 1;
-  static constexpr int nt = warps * 32;
-  static size_t smem() {
-    return sizeof(double2) * (2 * CAP * CAP + warps * (CAP * CAP + 2 * CAP * CAP));
-  }
+struct MmaCfg {
+  static constexpr int R8 = (CAP + 7) / 8 * 8;              // padded rows of env / T
+  static constexpr int L1 = (CAP + 15) / 16 * 16 + 4;       // env plane leading dim
+  static constexpr int L2 = (2 * CAP + 15) / 16 * 16 + 4;   // T plane leading dim
+  static constexpr int per_warp = 2 * R8 * L1 + 2 * R8 * L2;  // doubles
+  static constexpr int max_warps = (220 * 1024) / (per_warp * 8);
+  static constexpr int warps = max_warps > 16 ? 16 : (max_warps < 1 ? 1 : max_warps);
+  static constexpr size_t smem = sizeof(double) * (size_t)per_warp * warps;
 };
 
-struct O2Args {
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+struct CTile {  // complex 8x8 accumulator fragment: rows g, cols 2q, 2q+1
+  double r0, r1, i0, i1;
+};
+
+// acc += (ar + i ai) (br + i bi) on one 8x8x4 fragment
+__device__ __forceinline__ void cmma(CTile& c, double ar, double ai, double br, double bi) {
+  dmma(c.r0, c.r1, ar, br);
+  dmma(c.i0, c.i1, ar, bi);
+  dmma(c.r0, c.r1, -ai, bi);
+  dmma(c.i0, c.i1, ai, br);
+}
+
+struct MmaArgs {
   const double2* bra;
   const double2* ket;
   const int32_t* bra_chi;
@@ -334,55 +365,113 @@ struct O2Args {
 };
 
 template <int CAP>
-__global__ void __launch_bounds__(O2Cfg<CAP>::nt) overlap_o2_kernel(O2Args a) {
-  constexpr int NW = O2Cfg<CAP>::warps, NT = NW * 32;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* As = reinterpret_cast<double2*>(smem_raw);  // [al][p][ar] conj
+__global__ void __launch_bounds__(MmaCfg<CAP>::warps * 32, 1) overlap_mma_kernel(MmaArgs a) {
+  using C = MmaCfg<CAP>;
+  extern __shared__ __align__(16) double smem_d[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* env = As + 2 * CAP * CAP + warp * (3 * CAP * CAP);  // [al][kb], ld CAP
-  double2* T = env + CAP * CAP;                                 // [(al,p)][br], ld CAP
+  const int g = lane >> 2, q = lane & 3;  // fragment row group / thread in group
+  double* er = smem_d + (size_t)warp * C::per_warp;
+  double* ei = er + C::R8 * C::L1;
+  double* tr = ei + C::R8 * C::L1;
+  double* ti = tr + C::R8 * C::L2;
   const int m = a.m;
   const bool train = a.kind == MPSKQ_KIND_TRAIN;
   for (int64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
     const int2 tile = a.tiles[t];
     const int64_t i = tile.x;
-    const int64_t j = (int64_t)tile.y * NW + warp;
-    const bool valid = j < a.n_kets && (!train || i < j);
-    const int64_t jc = j < a.n_kets ? j : a.n_kets - 1;
+    const int64_t j = (int64_t)tile.y * C::warps + warp;
+    if (j >= a.n_kets || (train && i >= j)) continue;  // warps are independent
     const double2* bra = a.bra + i * a.stride;
-    const double2* ket = a.ket + jc * a.stride;
+    const double2* ket = a.ket + j * a.stride;
     const int32_t* bchi = a.bra_chi + i * (m + 1);
-    const int32_t* kchi = a.ket_chi + jc * (m + 1);
-    if (lane == 0) env[0] = make_double2(1.0, 0.0);
+    const int32_t* kchi = a.ket_chi + j * (m + 1);
+    for (int idx = lane; idx < 2 * C::R8 * C::L1; idx += 32) er[idx] = 0.0;
+    __syncwarp();
+    if (lane == 0) er[0] = 1.0;  // env = [[1]]
     __syncwarp();
     for (int s = 0; s < m; ++s) {
-      const int na = bchi[s], na1 = bchi[s + 1];
-      const int nb = kchi[s], nb1 = kchi[s + 1];
-      const double2* A = bra + a.site_off[s];
-      for (int idx = threadIdx.x; idx < na * 2 * na1; idx += NT) As[idx] = __ldg(A + idx);
-      __syncthreads();
-      const double2* B = ket + a.site_off[s];
-      // T[al][p][br] = sum_kb env[al][kb] B[kb][p][br]
-      for (int it = lane; it < na * 2 * nb1; it += 32) {
-        const int al = it / (2 * nb1), rem = it - al * 2 * nb1;
-        const int p = rem / nb1, br = rem - p * nb1;
-        double2 acc = cz();
-        for (int kb = 0; kb < nb; ++kb)
-          acc = cfma(env[al * CAP + kb], __ldg(B + (kb * 2 + p) * nb1 + br), acc);
-        T[(al * 2 + p) * CAP + br] = acc;
+      const int na = __ldg(bchi + s), na1 = __ldg(bchi + s + 1);
+      const int nb = __ldg(kchi + s), nb1 = __ldg(kchi + s + 1);
+      const double2* A = bra + __ldg(a.site_off + s);
+      const double2* B = ket + __ldg(a.site_off + s);
+      // ---- phase 1: T (na x 2nb1) = env (na x nb) . B (nb x 2nb1)
+      {
+        const int nt_n = (2 * nb1 + 7) >> 3, mt_n = (na + 7) >> 3, ks_n = (nb + 3) >> 2;
+        const int ncol = 2 * nb1;
+        for (int mt = 0; mt < mt_n; ++mt) {
+          for (int nt = 0; nt < nt_n; nt += 2) {
+            CTile c0{0, 0, 0, 0}, c1{0, 0, 0, 0};
+            const int n0 = nt * 8 + g, n1 = n0 + 8;
+            for (int ks = 0; ks < ks_n; ++ks) {
+              const int row = mt * 8 + g, kk = ks * 4 + q;
+              const double ar = er[row * C::L1 + kk], ai = ei[row * C::L1 + kk];
+              double2 b0 = make_double2(0.0, 0.0), b1 = make_double2(0.0, 0.0);
+              if (kk < nb) {
+                if (n0 < ncol) b0 = __ldg(B + kk * ncol + n0);
+                if (n1 < ncol) b1 = __ldg(B + kk * ncol + n1);
+              }
+              cmma(c0, ar, ai, b0.x, b0.y);
+              cmma(c1, ar, ai, b1.x, b1.y);
+            }
+            const int row = mt * 8 + g, col = nt * 8 + 2 * q;
+            tr[row * C::L2 + col] = c0.r0;
+            tr[row * C::L2 + col + 1] = c0.r1;
+            ti[row * C::L2 + col] = c0.i0;
+            ti[row * C::L2 + col + 1] = c0.i1;
+            if (nt + 1 < nt_n) {
+              tr[row * C::L2 + col + 8] = c1.r0;
+              tr[row * C::L2 + col + 9] = c1.r1;
+              ti[row * C::L2 + col + 8] = c1.i0;
+              ti[row * C::L2 + col + 9] = c1.i1;
+            }
+          }
+        }
       }
       __syncwarp();
-      // env[ar][br] = sum_{al,p} conj(A[al][p][ar]) T[al][p][br]
-      for (int it = lane; it < na1 * nb1; it += 32) {
-        const int ar = it / nb1, br = it - ar * nb1;
-        double2 acc = cz();
-        for (int q = 0; q < 2 * na; ++q) acc = cfmac(As[q * na1 + ar], T[q * CAP + br], acc);
-        env[ar * CAP + br] = acc;
+      // ---- phase 2: E' (na1 x nb1) = conj(A)^T (na1 x 2na) . T2 (2na x nb1)
+      {
+        const int nt_n = (nb1 + 7) >> 3, mt_n = (na1 + 7) >> 3, ks_n = (2 * na + 3) >> 2;
+        for (int mt = 0; mt < mt_n; ++mt) {
+          for (int nt = 0; nt < nt_n; nt += 2) {
+            CTile c0{0, 0, 0, 0}, c1{0, 0, 0, 0};
+            const int ar_ = mt * 8 + g;
+            const int n0 = nt * 8 + g, n1 = n0 + 8;
+            for (int ks = 0; ks < ks_n; ++ks) {
+              const int k = ks * 4 + q;  // (al, p) = (k >> 1, k & 1)
+              double2 av = make_double2(0.0, 0.0);
+              if (ar_ < na1 && k < 2 * na) av = __ldg(A + k * na1 + ar_);
+              // B fragment: T2[kb][n] with kb = ks*4 + q, n = column group g
+              const int kb = ks * 4 + q;
+              const int trow = kb >> 1, tcol = (kb & 1) * nb1;
+              double b0r = 0.0, b0i = 0.0, b1r = 0.0, b1i = 0.0;
+              if (n0 < nb1) {
+                b0r = tr[trow * C::L2 + tcol + n0];
+                b0i = ti[trow * C::L2 + tcol + n0];
+              }
+              if (n1 < nb1) {
+                b1r = tr[trow * C::L2 + tcol + n1];
+                b1i = ti[trow * C::L2 + tcol + n1];
+              }
+              cmma(c0, av.x, -av.y, b0r, b0i);  // conj(A)
+              cmma(c1, av.x, -av.y, b1r, b1i);
+            }
+            const int row = mt * 8 + g, col = nt * 8 + 2 * q;
+            er[row * C::L1 + col] = c0.r0;
+            er[row * C::L1 + col + 1] = c0.r1;
+            ei[row * C::L1 + col] = c0.i0;
+            ei[row * C::L1 + col + 1] = c0.i1;
+            if (nt + 1 < nt_n) {
+              er[row * C::L1 + col + 8] = c1.r0;
+              er[row * C::L1 + col + 9] = c1.r1;
+              ei[row * C::L1 + col + 8] = c1.i0;
+              ei[row * C::L1 + col + 9] = c1.i1;
+            }
+          }
+        }
       }
       __syncwarp();
-      __syncthreads();
     }
-    if (valid) store_result(a.out_mode, a.out, a.ld, i, j, env[0], train);
+    if (lane == 0) store_result(a.out_mode, a.out, a.ld, i, j, make_double2(er[0], ei[0]), train);
     __syncwarp();
   }
 }
@@ -429,13 +518,6 @@ std::vector<int2> make_tiles(bool train, int64_t n_rows, int64_t n_cols, int rb,
   return tiles;
 }
 
-int grid_for(int64_t n_tiles, int per_sm) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t cap = (int64_t)sms * per_sm * 64;
-  return (int)std::max<int64_t>(1, std::min(n_tiles, cap));
-}
 
 int launch_o1(const OverlapArgs& a, cudaStream_t st) {
   const int m = a.m;
@@ -485,38 +567,39 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
 }
 
 template <int CAP>
-int launch_o2(const OverlapArgs& a, cudaStream_t st) {
-  using C = O2Cfg<CAP>;
-  const size_t smem = C::smem();
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(overlap_o2_kernel<CAP>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(o2)");
-  }
+int launch_mma(const OverlapArgs& a, cudaStream_t st) {
+  using C = MmaCfg<CAP>;
+  cudaError_t e = cudaFuncSetAttribute(overlap_mma_kernel<CAP>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(mma)");
   const bool train = a.kind == MPSKQ_KIND_TRAIN;
   auto tiles = make_tiles(train, a.n_bras, a.n_kets, 1, C::warps, a.rank, a.world);
   int2* dtiles = nullptr;
   if (int s = upload_tiles(tiles, &dtiles, st)) return s;
   if (!tiles.empty()) {
-    O2Args o{reinterpret_cast<const double2*>(a.bra_sites),
-             reinterpret_cast<const double2*>(a.ket_sites),
-             a.bra_chi,
-             a.ket_chi,
-             a.site_off,
-             a.state_stride,
-             a.n_bras,
-             a.n_kets,
-             a.m,
-             a.kind,
-             a.out_mode,
-             dtiles,
-             (int64_t)tiles.size(),
-             a.out,
-             a.ld};
-    overlap_o2_kernel<CAP><<<grid_for((int64_t)tiles.size(), 4), C::nt, smem, st>>>(o);
+    MmaArgs o{reinterpret_cast<const double2*>(a.bra_sites),
+              reinterpret_cast<const double2*>(a.ket_sites),
+              a.bra_chi,
+              a.ket_chi,
+              a.site_off,
+              a.state_stride,
+              a.n_bras,
+              a.n_kets,
+              a.m,
+              a.kind,
+              a.out_mode,
+              dtiles,
+              (int64_t)tiles.size(),
+              a.out,
+              a.ld};
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = (int)std::min<int64_t>((int64_t)tiles.size(), (int64_t)sms * 16);
+    overlap_mma_kernel<CAP><<<grid, C::warps * 32, C::smem, st>>>(o);
   }
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "overlap_o2 launch");
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "overlap_mma launch");
   cudaFreeAsync(dtiles, st);
   return MPSKQ_OK;
 }
@@ -528,12 +611,12 @@ int launch_overlap(const OverlapArgs& a, void* stream) {
   int s = MPSKQ_OK;
   switch (a.chi_cap) {
     case 4: s = launch_o1(a, st); break;
-    case 8: s = launch_o2<8>(a, st); break;
-    case 12: s = launch_o2<12>(a, st); break;
-    case 16: s = launch_o2<16>(a, st); break;
-    case 24: s = launch_o2<24>(a, st); break;
-    case 32: s = launch_o2<32>(a, st); break;
-    case 48: s = launch_o2<48>(a, st); break;
+    case 8: s = launch_mma<8>(a, st); break;
+    case 12: s = launch_mma<12>(a, st); break;
+    case 16: s = launch_mma<16>(a, st); break;
+    case 24: s = launch_mma<24>(a, st); break;
+    case 32: s = launch_mma<32>(a, st); break;
+    case 48: s = launch_mma<48>(a, st); break;
     default: return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", a.chi_cap);
   }
   if (s != MPSKQ_OK) return s;
@@ -549,12 +632,12 @@ int launch_overlap(const OverlapArgs& a, void* stream) {
 void tile_shape(int chi_cap, int* rb, int* cb) {
   switch (chi_cap) {
     case 4: *rb = kWarpsO1; *cb = kLanes; return;
-    case 8: *rb = 1; *cb = O2Cfg<8>::warps; return;
-    case 12: *rb = 1; *cb = O2Cfg<12>::warps; return;
-    case 16: *rb = 1; *cb = O2Cfg<16>::warps; return;
-    case 24: *rb = 1; *cb = O2Cfg<24>::warps; return;
-    case 32: *rb = 1; *cb = O2Cfg<32>::warps; return;
-    default: *rb = 1; *cb = O2Cfg<48>::warps; return;
+    case 8: *rb = 1; *cb = MmaCfg<8>::warps; return;
+    case 12: *rb = 1; *cb = MmaCfg<12>::warps; return;
+    case 16: *rb = 1; *cb = MmaCfg<16>::warps; return;
+    case 24: *rb = 1; *cb = MmaCfg<24>::warps; return;
+    case 32: *rb = 1; *cb = MmaCfg<32>::warps; return;
+    default: *rb = 1; *cb = MmaCfg<48>::warps; return;
   }
 }
 
