@@ -32,6 +32,16 @@ __device__ constexpr double kNoiseFloor = 10.0 * DBL_EPSILON;
 __device__ constexpr double kInvSqrt2 = 0.7071067811865475;
 constexpr int kMaxSweeps = 40;
 
+// thread index within the state's thread group: NT == 32 kernels carry one
+// state per warp (several lockstepped warps per CTA), larger NT one per CTA
+template <int NT>
+__device__ __forceinline__ int ltid() {
+  if constexpr (NT == 32)
+    return threadIdx.x & 31;
+  else
+    return threadIdx.x;
+}
+
 template <int CAP>
 struct NtFor {
   static constexpr int value = CAP <= 4 ? 32 : CAP <= 8 ? 64 : CAP <= 16 ? 128 : CAP <= 32 ? 256 : 384;
@@ -63,7 +73,7 @@ struct Smem {
   int* chi;      // m + 1
   double4* rlog;  // per-CTA rotation log (capacities > 32 only)
 
-  static size_t bytes(int m) {
+  __host__ __device__ static size_t bytes(int m) {
     size_t b = sizeof(double2) * ((LogW<CAP>::value ? 1 : 2) * LD * LD + 2 * CAP * CAP + LD);
     b += sizeof(double) * (2 * LD + 32 + 4);
     b += sizeof(int) * (LD + 4 + m + 1);
@@ -115,7 +125,7 @@ __device__ void apply_reflector(double2* M, const double2* u, double tau, int j,
   if (nc <= 0 || tau == 0.0) return;
   const int G = group_width<NT>(nc);
   const int per = NT / G;
-  const int tid = threadIdx.x;
+  const int tid = ltid<NT>();
   for (int base = 0; base < nc; base += per) {
     const int ci = base + tid / G, g = tid % G;
     const bool act = ci < nc;
@@ -136,7 +146,7 @@ __device__ void apply_reflector(double2* M, const double2* u, double tau, int j,
 template <int CAP, int NT>
 __device__ __noinline__ int householder_qr(Smem<CAP, NT>& sm, int Rr, int Cc) {
   constexpr int LD = 2 * CAP;
-  const int tid = threadIdx.x;
+  const int tid = ltid<NT>();
   const int k = min(Rr, Cc);
   double2* A = sm.A;
   for (int j = 0; j < k; ++j) {
@@ -199,7 +209,7 @@ template <int CAP, int NT, int G>
 __device__ __noinline__ int jacobi_sweeps(Smem<CAP, NT>& sm, int Rr, int n) {
   constexpr bool kLog = LogW<CAP>::value;
   constexpr int LD = 2 * CAP;
-  const int tid = threadIdx.x;
+  const int tid = ltid<NT>();
   double2* A = sm.A;
   double2* W = sm.W;
   const int ne = n + (n & 1), P = ne >> 1, span = ne - 1;
@@ -287,7 +297,7 @@ __device__ __noinline__ int jacobi_sweeps(Smem<CAP, NT>& sm, int Rr, int n) {
 template <int CAP, int NT, int G>
 __device__ __noinline__ void replay_sweeps(Smem<CAP, NT>& sm, double2* Wm, int n, int sweeps) {
   constexpr int LD = 2 * CAP;
-  const int tid = threadIdx.x;
+  const int tid = ltid<NT>();
   const int ne = n + (n & 1), P = ne >> 1, span = ne - 1;
   const int k = tid / G, g = tid % G;
   for (int sweep = 0; sweep < sweeps; ++sweep) {
@@ -328,7 +338,7 @@ template <int CAP, int NT>
 __device__ void init_identity(double2* Wm, int n) {
   constexpr int LD = 2 * CAP;
   #pragma unroll 1
-  for (int idx = threadIdx.x; idx < n * n; idx += NT) {
+  for (int idx = ltid<NT>(); idx < n * n; idx += NT) {
     const int c = idx / n, r = idx - c * n;
     Wm[c * LD + r] = make_double2(r == c ? 1.0 : 0.0, 0.0);
   }
@@ -366,7 +376,7 @@ __device__ void replay(Smem<CAP, NT>& sm, double2* Wm, int n, int sweeps) {
 template <int CAP, int NT>
 __device__ __noinline__ void norms_and_order(Smem<CAP, NT>& sm, int Rr, int n) {
   constexpr int LD = 2 * CAP;
-  const int tid = threadIdx.x;
+  const int tid = ltid<NT>();
   const int G = group_width<NT>(n);
   const int per = NT / G;
   for (int base = 0; base < n; base += per) {
@@ -444,7 +454,7 @@ __device__ void op_one_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, d
   double2* p = st.base + st.off[q];
   const int n = chl * chr;
   #pragma unroll 1
-  for (int idx = threadIdx.x; idx < n; idx += NT) {
+  for (int idx = ltid<NT>(); idx < n; idx += NT) {
     const int a = idx / chr, b = idx - a * chr;
     const int i0 = (2 * a) * chr + b, i1 = i0 + chr;
     const double2 x0 = p[i0], x1 = p[i1];
@@ -470,7 +480,7 @@ __device__ void op_one_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, d
 template <int CAP, int NT>
 __device__ void op_qr_left(Smem<CAP, NT>& sm, StateCtx& st, int i) {
   constexpr int LD = 2 * CAP;
-  const int tid = threadIdx.x;
+  const int tid = ltid<NT>();
   const int chl = sm.chi[i], chr = sm.chi[i + 1], chn = sm.chi[i + 2];
   double2* M = st.base + st.off[i];
   double2* N = st.base + st.off[i + 1];
@@ -509,7 +519,7 @@ __device__ void op_qr_left(Smem<CAP, NT>& sm, StateCtx& st, int i) {
 template <int CAP, int NT>
 __device__ void op_qr_right(Smem<CAP, NT>& sm, StateCtx& st, int i) {
   constexpr int LD = 2 * CAP;
-  const int tid = threadIdx.x;
+  const int tid = ltid<NT>();
   const int chp = sm.chi[i - 1], chl = sm.chi[i], chr = sm.chi[i + 1];
   double2* M = st.base + st.off[i];
   double2* P = st.base + st.off[i - 1];
@@ -549,7 +559,7 @@ template <int CAP, int NT>
 __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, bool left,
                              double2 cs, double budget, int chi_max) {
   constexpr int LD = 2 * CAP;
-  const int tid = threadIdx.x;
+  const int tid = ltid<NT>();
   const int chl = sm.chi[q], chm = sm.chi[q + 1], chr = sm.chi[q + 2];
   double2* X = st.base + st.off[q];
   double2* Y = st.base + st.off[q + 1];
@@ -671,63 +681,82 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
 
 
 // ---------------------------------------------------------------------------
+// States per CTA: NT == 32 kernels run SPC states (one per warp) in lockstep,
+// a CTA barrier after every op, so the SM's warps stay in the same small
+// region of the (large) op code and the instruction cache keeps up.
+template <int NT>
+struct SpcFor {
+  static constexpr int value = NT == 32 ? 4 : 1;
+};
+
 template <int CAP, int NT>
-__global__ void __launch_bounds__(NT) sim_kernel(SimArgs a) {
+__global__ void __launch_bounds__(NT * SpcFor<NT>::value) sim_kernel(SimArgs a) {
+  constexpr int SPC = SpcFor<NT>::value;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int slot = SPC > 1 ? (int)(threadIdx.x >> 5) : 0;
   Smem<CAP, NT> sm;
-  sm.carve(smem_raw, a.m);
+  sm.carve(smem_raw + (size_t)slot * Smem<CAP, NT>::bytes(a.m), a.m);
   if constexpr (LogW<CAP>::value)
     sm.rlog = static_cast<double4*>(a.scratch) + (int64_t)blockIdx.x * LogW<CAP>::entries;
-  const int tid = threadIdx.x;
+  const int tid = ltid<NT>();
   const int m = a.m;
   const int4* ops = reinterpret_cast<const int4*>(a.ops);
   const double2* coef = reinterpret_cast<const double2*>(a.coef);
-  for (int64_t n = blockIdx.x; n < a.n_states; n += gridDim.x) {
-    StateCtx st{reinterpret_cast<double2*>(a.sites) + n * a.state_stride, a.site_off, m,
+  for (int64_t n0 = (int64_t)blockIdx.x * SPC; n0 < a.n_states; n0 += (int64_t)gridDim.x * SPC) {
+    const int64_t n = n0 + slot;
+    bool live = n < a.n_states;  // uniform per state group
+    StateCtx st{reinterpret_cast<double2*>(a.sites) + (live ? n : 0) * a.state_stride, a.site_off, m,
                 MPSKQ_STATE_OK, 1, 0.0};
-    // init_state(m, "zero"): every site (1, 2, 1) = [1, 0]  (mps.py:90-102)
-    #pragma unroll 1
-    for (int b = tid; b <= m; b += NT) sm.chi[b] = 1;
-    #pragma unroll 1
-    for (int s = tid; s < m; s += NT) {
-      st.base[a.site_off[s]] = make_double2(1.0, 0.0);
-      st.base[a.site_off[s] + 1] = cz();
+    if (live) {
+      // init_state(m, "zero"): every site (1, 2, 1) = [1, 0]  (mps.py:90-102)
+      #pragma unroll 1
+      for (int b = tid; b <= m; b += NT) sm.chi[b] = 1;
+      #pragma unroll 1
+      for (int s = tid; s < m; s += NT) {
+        st.base[a.site_off[s]] = make_double2(1.0, 0.0);
+        st.base[a.site_off[s] + 1] = cz();
+      }
+      bsync<NT>();
     }
-    bsync<NT>();
-    const double2* cf = coef + n * a.n_params;
+    const double2* cf = coef + (live ? n : 0) * a.n_params;
     for (int64_t i = 0; i < a.n_ops; ++i) {
-      const int4 op = __ldg(ops + i);
-      const int code = op.x & 0xff;
-      const bool left = (op.x >> 8) & MPSKQ_ABSORB_LEFT;
-      const double2 cs = op.z >= 0 ? __ldg(cf + op.z) : make_double2(1.0, 0.0);
-      switch (code) {
-        case MPSKQ_OP_H:
-        case MPSKQ_OP_RZ:
-          op_one_qubit<CAP, NT>(sm, st, op.y, code, cs);
-          break;
-        case MPSKQ_OP_QRL:
-          op_qr_left<CAP, NT>(sm, st, op.y);
-          break;
-        case MPSKQ_OP_QRR:
-          op_qr_right<CAP, NT>(sm, st, op.y);
-          break;
-        default:
-          op_two_qubit<CAP, NT>(sm, st, op.y, code, left, cs, a.budget, a.chi_max);
-          break;
+      if (live) {
+        const int4 op = __ldg(ops + i);
+        const int code = op.x & 0xff;
+        const bool left = (op.x >> 8) & MPSKQ_ABSORB_LEFT;
+        const double2 cs = op.z >= 0 ? __ldg(cf + op.z) : make_double2(1.0, 0.0);
+        switch (code) {
+          case MPSKQ_OP_H:
+          case MPSKQ_OP_RZ:
+            op_one_qubit<CAP, NT>(sm, st, op.y, code, cs);
+            break;
+          case MPSKQ_OP_QRL:
+            op_qr_left<CAP, NT>(sm, st, op.y);
+            break;
+          case MPSKQ_OP_QRR:
+            op_qr_right<CAP, NT>(sm, st, op.y);
+            break;
+          default:
+            op_two_qubit<CAP, NT>(sm, st, op.y, code, left, cs, a.budget, a.chi_max);
+            break;
+        }
+        if (st.status != MPSKQ_STATE_OK) live = false;  // keep hitting the barriers
+        if (live && a.entry_log != nullptr && op.w >= 0 && tid == 0) {
+          int64_t entries = 0;
+          for (int s = 0; s < m; ++s) entries += 2 * (int64_t)sm.chi[s] * sm.chi[s + 1];
+          a.entry_log[n * a.n_gates + op.w] = entries;
+        }
       }
-      if (st.status != MPSKQ_STATE_OK) break;
-      if (a.entry_log != nullptr && op.w >= 0 && tid == 0) {
-        int64_t entries = 0;
-        for (int s = 0; s < m; ++s) entries += 2 * (int64_t)sm.chi[s] * sm.chi[s + 1];
-        a.entry_log[n * a.n_gates + op.w] = entries;
-      }
+      if constexpr (SPC > 1) __syncthreads();
     }
-    #pragma unroll 1
-    for (int b = tid; b <= m; b += NT) a.chi[n * (m + 1) + b] = sm.chi[b];
-    if (tid == 0) {
-      a.discard[n] = st.discard;
-      a.peak[n] = st.peak;
-      a.status[n] = st.status;
+    if (n < a.n_states) {
+      #pragma unroll 1
+      for (int b = tid; b <= m; b += NT) a.chi[n * (m + 1) + b] = sm.chi[b];
+      if (tid == 0) {
+        a.discard[n] = st.discard;
+        a.peak[n] = st.peak;
+        a.status[n] = st.status;
+      }
     }
     bsync<NT>();
   }
@@ -742,7 +771,7 @@ __global__ void __launch_bounds__(NT) svd_kernel(SvdArgs a) {
   sm.carve(smem_raw, 0);
   if constexpr (LogW<CAP>::value)
     sm.rlog = static_cast<double4*>(a.scratch) + (int64_t)blockIdx.x * LogW<CAP>::entries;
-  const int tid = threadIdx.x;
+  const int tid = ltid<NT>();
   const int rows = a.rows, cols = a.cols, kmin = min(rows, cols);
   for (int64_t b = blockIdx.x; b < a.batch; b += gridDim.x) {
     const double2* M = reinterpret_cast<const double2*>(a.mats) + b * rows * cols;
@@ -828,12 +857,13 @@ int plan_grid(int64_t items, cudaStream_t st, int64_t* grid, void** scratch) {
 template <int CAP>
 int launch_sim_cap(const SimArgs& a0, cudaStream_t st) {
   constexpr int NT = NtFor<CAP>::value;
-  const size_t smem = Smem<CAP, NT>::bytes(a0.m);
+  constexpr int SPC = SpcFor<NT>::value;
+  const size_t smem = Smem<CAP, NT>::bytes(a0.m) * SPC;
   if (int s = prepare(sim_kernel<CAP, NT>, smem)) return s;
   SimArgs a = a0;
   int64_t grid = 0;
-  if (int s = plan_grid<CAP>(a.n_states, st, &grid, &a.scratch)) return s;
-  sim_kernel<CAP, NT><<<(unsigned)grid, NT, smem, st>>>(a);
+  if (int s = plan_grid<CAP>((a.n_states + SPC - 1) / SPC, st, &grid, &a.scratch)) return s;
+  sim_kernel<CAP, NT><<<(unsigned)grid, NT * SPC, smem, st>>>(a);
   cudaError_t e = cudaGetLastError();
   if (a.scratch) cudaFreeAsync(a.scratch, st);
   if (e != cudaSuccess) return cuda_fail(e, "sim_kernel launch");
