@@ -205,6 +205,28 @@ __device__ __forceinline__ double gsum(double v) {
   return v;
 }
 
+// round-robin pair of group k in round t (circle method: position 0 fixed,
+// positions 1..ne-1 rotate by t); p < q
+__device__ __forceinline__ void rr_pair(int k, int t, int ne, int& p, int& q) {
+  const int span = ne - 1;
+  const int pa = k, pb = ne - 1 - k;
+  int x = pa - 1 + t, y = pb - 1 + t;
+  x = x >= span ? x - span : x;
+  y = y >= span ? y - span : y;
+  p = pa == 0 ? 0 : 1 + x;
+  q = 1 + y;
+  if (p > q) {
+    const int tmp = p;
+    p = q;
+    q = tmp;
+  }
+}
+
+// Returns the number of rounds run (the log-mode replay repeats them).  The
+// iteration stops once a full cycle of rounds (every pair once) has made no
+// rotation, even mid-sweep.  (Tracking the column norms through rotations
+// instead of recomputing them stalls convergence on the noise columns of
+// rank-deficient thetas, so the norms are recomputed every round.)
 template <int CAP, int NT, int G>
 __device__ __noinline__ int jacobi_sweeps(Smem<CAP, NT>& sm, int Rr, int n) {
   constexpr bool kLog = LogW<CAP>::value;
@@ -217,120 +239,91 @@ __device__ __noinline__ int jacobi_sweeps(Smem<CAP, NT>& sm, int Rr, int n) {
   // convergence: |c_p^H c_q| <= tol * |c_p| |c_q|, compared in squares
   const double tol = DBL_EPSILON * (double)max(Rr, 8);
   const double tol2 = tol * tol;
-  int sweep = 0;
-  while (sweep < kMaxSweeps) {
-    int rotated = 0;
-    for (int t = 0; t < span; ++t) {
-      // circle method: position 0 is fixed, positions 1..ne-1 rotate by t
-      int p = 0, q = 0;
-      if (k < P) {
-        const int pa = k, pb = ne - 1 - k;
-        int x = pa - 1 + t, y = pb - 1 + t;
-        x = x >= span ? x - span : x;
-        y = y >= span ? y - span : y;
-        p = pa == 0 ? 0 : 1 + x;
-        q = 1 + y;
-        if (p > q) {
-          const int tmp = p;
-          p = q;
-          q = tmp;
-        }
+  const int max_rounds = kMaxSweeps * span;
+  int round = 0, quiet = 0;
+  for (; round < max_rounds;) {
+    const int t = round % span;
+    int p = 0, q = 0;
+    if (k < P) rr_pair(k, t, ne, p, q);
+    const bool act = k < P && q < n;
+    double a = 0.0, b = 0.0, gx = 0.0, gy = 0.0;
+    if (act) {
+      #pragma unroll 1
+      for (int r = g; r < Rr; r += G) {
+        const double2 x = A[p * LD + r], y = A[q * LD + r];
+        a = fma(x.x, x.x, fma(x.y, x.y, a));
+        b = fma(y.x, y.x, fma(y.y, y.y, b));
+        gx = fma(x.x, y.x, fma(x.y, y.y, gx));
+        gy = fma(x.x, y.y, fma(-x.y, y.x, gy));
       }
-      const bool act = k < P && q < n;
-      double a = 0.0, b = 0.0, gx = 0.0, gy = 0.0;
-      if (act) {
-        #pragma unroll 1
-        for (int r = g; r < Rr; r += G) {
-          const double2 x = A[p * LD + r], y = A[q * LD + r];
-          a = fma(x.x, x.x, fma(x.y, x.y, a));
-          b = fma(y.x, y.x, fma(y.y, y.y, b));
-          gx = fma(x.x, y.x, fma(x.y, y.y, gx));
-          gy = fma(x.x, y.y, fma(-x.y, y.x, gy));
-        }
-      }
-      a = gsum<G>(a);
-      b = gsum<G>(b);
-      gx = gsum<G>(gx);
-      gy = gsum<G>(gy);
-      const double g2 = fma(gx, gx, gy * gy);
-      const bool rot = act && g2 > tol2 * a * b && g2 > 0.0;
-      double4* entry = nullptr;
-      if constexpr (kLog) entry = sm.rlog + ((int64_t)sweep * span + t) * P + k;
-      if (kLog && act && g == 0 && !rot) *entry = make_double4(1.0, 0.0, 0.0, 0.0);
-      if (rot) {
-        rotated = 1;
-        const double inv = rsqrt(g2);  // 1/|gamma|
-        const double zeta = (b - a) * (0.5 * inv);
-        const double az = fabs(zeta);
-        const double tt = az > 1e150 ? 0.5 / az : 1.0 / (az + sqrt(fma(zeta, zeta, 1.0)));
-        const double t_ = copysign(tt, zeta);
-        const double c = rsqrt(fma(t_, t_, 1.0));
-        const double sn = c * t_;
-        // [x', y'] = [x, y] J,  J = [[c, s e], [-s conj(e), c]],  e = gamma/|gamma|
-        const double2 se = make_double2(sn * gx * inv, sn * gy * inv);
-        #pragma unroll 1
-        for (int r = g; r < Rr; r += G) {
-          const double2 x = A[p * LD + r], y = A[q * LD + r];
-          A[p * LD + r] = csub(cscale(x, c), cmul(cconj(se), y));
-          A[q * LD + r] = cadd(cmul(se, x), cscale(y, c));
-        }
-        if constexpr (kLog) {
-          if (g == 0) *entry = make_double4(c, se.x, se.y, 1.0);
-        } else {
-          #pragma unroll 1
-          for (int r = g; r < n; r += G) {
-            const double2 x = W[p * LD + r], y = W[q * LD + r];
-            W[p * LD + r] = csub(cscale(x, c), cmul(cconj(se), y));
-            W[q * LD + r] = cadd(cmul(se, x), cscale(y, c));
-          }
-        }
-      }
-      bsync<NT>();
     }
-    ++sweep;
-    if (!block_any<NT>(rotated)) break;
+    a = gsum<G>(a);
+    b = gsum<G>(b);
+    gx = gsum<G>(gx);
+    gy = gsum<G>(gy);
+    const double g2 = fma(gx, gx, gy * gy);
+    const bool rot = act && g2 > tol2 * a * b && g2 > 0.0;
+    double4* entry = nullptr;
+    if constexpr (kLog) entry = sm.rlog + (int64_t)round * P + k;
+    if (kLog && act && g == 0 && !rot) *entry = make_double4(1.0, 0.0, 0.0, 0.0);
+    if (rot) {
+      const double inv = rsqrt(g2);  // 1/|gamma|
+      const double zeta = (b - a) * (0.5 * inv);
+      const double az = fabs(zeta);
+      const double tt = az > 1e150 ? 0.5 / az : 1.0 / (az + sqrt(fma(zeta, zeta, 1.0)));
+      const double t_ = copysign(tt, zeta);
+      const double c = rsqrt(fma(t_, t_, 1.0));
+      const double sn = c * t_;
+      // [x', y'] = [x, y] J,  J = [[c, s e], [-s conj(e), c]],  e = gamma/|gamma|
+      const double2 se = make_double2(sn * gx * inv, sn * gy * inv);
+      #pragma unroll 1
+      for (int r = g; r < Rr; r += G) {
+        const double2 x = A[p * LD + r], y = A[q * LD + r];
+        A[p * LD + r] = csub(cscale(x, c), cmul(cconj(se), y));
+        A[q * LD + r] = cadd(cmul(se, x), cscale(y, c));
+      }
+      if constexpr (kLog) {
+        if (g == 0) *entry = make_double4(c, se.x, se.y, 1.0);
+      } else {
+        #pragma unroll 1
+        for (int r = g; r < n; r += G) {
+          const double2 x = W[p * LD + r], y = W[q * LD + r];
+          W[p * LD + r] = csub(cscale(x, c), cmul(cconj(se), y));
+          W[q * LD + r] = cadd(cmul(se, x), cscale(y, c));
+        }
+      }
+    }
+    ++round;
+    quiet = block_any<NT>(rot) ? 0 : quiet + 1;
+    if (quiet >= span) break;
   }
-  return sweep;
+  return round;
 }
 
 // Log mode: W = I_n in `Wm`, then apply the logged rotations in order.
 template <int CAP, int NT, int G>
-__device__ __noinline__ void replay_sweeps(Smem<CAP, NT>& sm, double2* Wm, int n, int sweeps) {
+__device__ __noinline__ void replay_sweeps(Smem<CAP, NT>& sm, double2* Wm, int n, int rounds) {
   constexpr int LD = 2 * CAP;
   const int tid = ltid<NT>();
   const int ne = n + (n & 1), P = ne >> 1, span = ne - 1;
   const int k = tid / G, g = tid % G;
-  for (int sweep = 0; sweep < sweeps; ++sweep) {
-    for (int t = 0; t < span; ++t) {
-      int p = 0, q = 0;
-      if (k < P) {
-        const int pa = k, pb = ne - 1 - k;
-        int x = pa - 1 + t, y = pb - 1 + t;
-        x = x >= span ? x - span : x;
-        y = y >= span ? y - span : y;
-        p = pa == 0 ? 0 : 1 + x;
-        q = 1 + y;
-        if (p > q) {
-          const int tmp = p;
-          p = q;
-          q = tmp;
+  for (int round = 0; round < rounds; ++round) {
+    int p = 0, q = 0;
+    if (k < P) rr_pair(k, round % span, ne, p, q);
+    if (k < P && q < n) {
+      const double4 e = sm.rlog[(int64_t)round * P + k];
+      if (e.w != 0.0) {
+        const double c = e.x;
+        const double2 se = make_double2(e.y, e.z);
+        #pragma unroll 1
+        for (int r = g; r < n; r += G) {
+          const double2 x = Wm[p * LD + r], y = Wm[q * LD + r];
+          Wm[p * LD + r] = csub(cscale(x, c), cmul(cconj(se), y));
+          Wm[q * LD + r] = cadd(cmul(se, x), cscale(y, c));
         }
       }
-      if (k < P && q < n) {
-        const double4 e = sm.rlog[((int64_t)sweep * span + t) * P + k];
-        if (e.w != 0.0) {
-          const double c = e.x;
-          const double2 se = make_double2(e.y, e.z);
-          #pragma unroll 1
-          for (int r = g; r < n; r += G) {
-            const double2 x = Wm[p * LD + r], y = Wm[q * LD + r];
-            Wm[p * LD + r] = csub(cscale(x, c), cmul(cconj(se), y));
-            Wm[q * LD + r] = cadd(cmul(se, x), cscale(y, c));
-          }
-        }
-      }
-      bsync<NT>();
     }
+    bsync<NT>();
   }
 }
 
@@ -345,7 +338,7 @@ __device__ void init_identity(double2* Wm, int n) {
   bsync<NT>();
 }
 
-// returns the number of sweeps run (needed by the log-mode replay)
+// returns the number of rounds run (needed by the log-mode replay)
 template <int CAP, int NT>
 __device__ int jacobi(Smem<CAP, NT>& sm, int Rr, int n) {
   if constexpr (!LogW<CAP>::value) init_identity<CAP, NT>(sm.W, n);
