@@ -327,9 +327,12 @@ struct MmaCfg {
   static constexpr int L1 = (CAP + 15) / 16 * 16 + 4;       // env plane leading dim
   static constexpr int L2 = (2 * CAP + 15) / 16 * 16 + 4;   // T plane leading dim
   static constexpr int per_warp = 2 * R8 * L1 + 2 * R8 * L2;  // doubles
+  // above ~200 KB per warp (capacities > 48) the planes move to a per-warp
+  // global scratch (L2 resident)
+  static constexpr bool global = (size_t)per_warp * 8 > 200 * 1024;
   static constexpr int max_warps = (220 * 1024) / (per_warp * 8);
-  static constexpr int warps = max_warps > 16 ? 16 : (max_warps < 1 ? 1 : max_warps);
-  static constexpr size_t smem = sizeof(double) * (size_t)per_warp * warps;
+  static constexpr int warps = global ? 4 : (max_warps > 16 ? 16 : (max_warps < 1 ? 1 : max_warps));
+  static constexpr size_t smem = global ? 0 : sizeof(double) * (size_t)per_warp * warps;
 };
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -362,6 +365,7 @@ struct MmaArgs {
   int64_t n_tiles;
   double* out;
   int64_t ld;
+  double* gws;  // per-warp planes for capacities whose planes exceed shared memory
 };
 
 template <int CAP>
@@ -370,7 +374,8 @@ __global__ void __launch_bounds__(MmaCfg<CAP>::warps * 32, 1) overlap_mma_kernel
   extern __shared__ __align__(16) double smem_d[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;  // fragment row group / thread in group
-  double* er = smem_d + (size_t)warp * C::per_warp;
+  double* er = (C::global ? a.gws + ((size_t)blockIdx.x * C::warps) * C::per_warp : smem_d) +
+               (size_t)warp * C::per_warp;
   double* ei = er + C::R8 * C::L1;
   double* tr = ei + C::R8 * C::L1;
   double* ti = tr + C::R8 * C::L2;
@@ -569,9 +574,12 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
 template <int CAP>
 int launch_mma(const OverlapArgs& a, cudaStream_t st) {
   using C = MmaCfg<CAP>;
-  cudaError_t e = cudaFuncSetAttribute(overlap_mma_kernel<CAP>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(mma)");
+  cudaError_t e = cudaSuccess;
+  if (C::smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(overlap_mma_kernel<CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)C::smem);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(mma)");
+  }
   const bool train = a.kind == MPSKQ_KIND_TRAIN;
   auto tiles = make_tiles(train, a.n_bras, a.n_kets, 1, C::warps, a.rank, a.world);
   int2* dtiles = nullptr;
@@ -591,12 +599,19 @@ int launch_mma(const OverlapArgs& a, cudaStream_t st) {
               dtiles,
               (int64_t)tiles.size(),
               a.out,
-              a.ld};
+              a.ld,
+              nullptr};
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = (int)std::min<int64_t>((int64_t)tiles.size(), (int64_t)sms * 16);
+    const int grid = (int)std::min<int64_t>((int64_t)tiles.size(), (int64_t)sms * (C::global ? 2 : 16));
+    if (C::global) {
+      e = cudaMallocAsync(reinterpret_cast<void**>(&o.gws),
+                          sizeof(double) * (size_t)C::per_warp * C::warps * grid, st);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(mma planes)");
+    }
     overlap_mma_kernel<CAP><<<grid, C::warps * 32, C::smem, st>>>(o);
+    if (o.gws) cudaFreeAsync(o.gws, st);
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "overlap_mma launch");
@@ -617,6 +632,9 @@ int launch_overlap(const OverlapArgs& a, void* stream) {
     case 24: s = launch_mma<24>(a, st); break;
     case 32: s = launch_mma<32>(a, st); break;
     case 48: s = launch_mma<48>(a, st); break;
+    case 64: s = launch_mma<64>(a, st); break;
+    case 80: s = launch_mma<80>(a, st); break;
+    case 96: s = launch_mma<96>(a, st); break;
     default: return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", a.chi_cap);
   }
   if (s != MPSKQ_OK) return s;
@@ -637,7 +655,10 @@ void tile_shape(int chi_cap, int* rb, int* cb) {
     case 16: *rb = 1; *cb = MmaCfg<16>::warps; return;
     case 24: *rb = 1; *cb = MmaCfg<24>::warps; return;
     case 32: *rb = 1; *cb = MmaCfg<32>::warps; return;
-    default: *rb = 1; *cb = MmaCfg<48>::warps; return;
+    case 48: *rb = 1; *cb = MmaCfg<48>::warps; return;
+    case 64: *rb = 1; *cb = MmaCfg<64>::warps; return;
+    case 80: *rb = 1; *cb = MmaCfg<80>::warps; return;
+    default: *rb = 1; *cb = MmaCfg<96>::warps; return;
   }
 }
 

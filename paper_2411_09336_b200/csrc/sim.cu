@@ -44,7 +44,17 @@ __device__ __forceinline__ int ltid() {
 
 template <int CAP>
 struct NtFor {
-  static constexpr int value = CAP <= 4 ? 32 : CAP <= 8 ? 64 : CAP <= 16 ? 128 : CAP <= 32 ? 256 : 384;
+  static constexpr int value =
+      CAP <= 4 ? 32 : CAP <= 8 ? 64 : CAP <= 16 ? 128 : CAP <= 32 ? 256 : CAP <= 48 ? 384 : 512;
+};
+
+// Capacities above 48: theta/C and the staging buffer no longer fit shared
+// memory; they live in a per-CTA global scratch (L2 resident), the small
+// per-op arrays stay in shared memory.
+template <int CAP>
+struct GlobalWs {
+  static constexpr bool value = CAP > 48;
+  static constexpr int64_t complexes = (int64_t)(2 * CAP) * (2 * CAP) + 2 * (int64_t)CAP * CAP;
 };
 
 // Capacities above 32 keep only theta/C in shared memory: the Jacobi rotations
@@ -74,22 +84,31 @@ struct Smem {
   double4* rlog;  // per-CTA rotation log (capacities > 32 only)
 
   __host__ __device__ static size_t bytes(int m) {
-    size_t b = sizeof(double2) * ((LogW<CAP>::value ? 1 : 2) * LD * LD + 2 * CAP * CAP + LD);
+    size_t b = GlobalWs<CAP>::value
+                   ? sizeof(double2) * LD
+                   : sizeof(double2) * ((LogW<CAP>::value ? 1 : 2) * LD * LD + 2 * CAP * CAP + LD);
     b += sizeof(double) * (2 * LD + 32 + 4);
     b += sizeof(int) * (LD + 4 + m + 1);
     return (b + 15) & ~size_t(15);
   }
-  __device__ void carve(void* base, int m) {
+  // gws: this CTA's global workspace (capacities > 48 only)
+  __device__ void carve(void* base, int m, double2* gws = nullptr) {
     char* p = static_cast<char*>(base);
-    A = reinterpret_cast<double2*>(p);
-    p += sizeof(double2) * LD * LD;
-    if constexpr (!LogW<CAP>::value) {
-      W = reinterpret_cast<double2*>(p);
+    if constexpr (GlobalWs<CAP>::value) {
+      A = gws;
+      S = gws + LD * LD;
+      W = S;
+    } else {
+      A = reinterpret_cast<double2*>(p);
       p += sizeof(double2) * LD * LD;
+      if constexpr (!LogW<CAP>::value) {
+        W = reinterpret_cast<double2*>(p);
+        p += sizeof(double2) * LD * LD;
+      }
+      S = reinterpret_cast<double2*>(p);
+      if constexpr (LogW<CAP>::value) W = S;  // Q of a QR move (Rr x k <= 2CAP x CAP)
+      p += sizeof(double2) * 2 * CAP * CAP;
     }
-    S = reinterpret_cast<double2*>(p);
-    if constexpr (LogW<CAP>::value) W = S;  // Q of a QR move (Rr x k <= 2CAP x CAP)
-    p += sizeof(double2) * 2 * CAP * CAP;
     rd = reinterpret_cast<double2*>(p);
     p += sizeof(double2) * LD;
     tau = reinterpret_cast<double*>(p);
@@ -343,12 +362,13 @@ template <int CAP, int NT>
 __device__ int jacobi(Smem<CAP, NT>& sm, int Rr, int n) {
   if constexpr (!LogW<CAP>::value) init_identity<CAP, NT>(sm.W, n);
   if (n < 2) return 0;
-  // lanes per column pair: G * (n/2) <= NT, G in {8, 16, 32} for every
-  // (CAP, NT) instantiation (NT >= 8 * CAP)
+  // lanes per column pair: G * (n/2) <= NT, G in {4, 8, 16, 32} for every
+  // (CAP, NT) instantiation (NT >= 4 * CAP)
   const int G = group_width<NT>((n + 1) >> 1);
   if (G >= 32) return jacobi_sweeps<CAP, NT, 32>(sm, Rr, n);
   if (G == 16) return jacobi_sweeps<CAP, NT, 16>(sm, Rr, n);
-  return jacobi_sweeps<CAP, NT, 8>(sm, Rr, n);
+  if (G == 8) return jacobi_sweeps<CAP, NT, 8>(sm, Rr, n);
+  return jacobi_sweeps<CAP, NT, 4>(sm, Rr, n);
 }
 
 // log mode: rebuild W (n x n) in Wm from the rotation log
@@ -361,8 +381,10 @@ __device__ void replay(Smem<CAP, NT>& sm, double2* Wm, int n, int sweeps) {
     replay_sweeps<CAP, NT, 32>(sm, Wm, n, sweeps);
   else if (G == 16)
     replay_sweeps<CAP, NT, 16>(sm, Wm, n, sweeps);
-  else
+  else if (G == 8)
     replay_sweeps<CAP, NT, 8>(sm, Wm, n, sweeps);
+  else
+    replay_sweeps<CAP, NT, 4>(sm, Wm, n, sweeps);
 }
 
 // column norms of C, descending order in perm (ties keep index order)
@@ -688,7 +710,12 @@ __global__ void __launch_bounds__(NT * SpcFor<NT>::value) sim_kernel(SimArgs a) 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int slot = SPC > 1 ? (int)(threadIdx.x >> 5) : 0;
   Smem<CAP, NT> sm;
-  sm.carve(smem_raw + (size_t)slot * Smem<CAP, NT>::bytes(a.m), a.m);
+  double2* gws = nullptr;
+  if constexpr (GlobalWs<CAP>::value)
+    gws = reinterpret_cast<double2*>(static_cast<double4*>(a.scratch) +
+                                     (int64_t)gridDim.x * LogW<CAP>::entries) +
+          (int64_t)blockIdx.x * GlobalWs<CAP>::complexes;
+  sm.carve(smem_raw + (size_t)slot * Smem<CAP, NT>::bytes(a.m), a.m, gws);
   if constexpr (LogW<CAP>::value)
     sm.rlog = static_cast<double4*>(a.scratch) + (int64_t)blockIdx.x * LogW<CAP>::entries;
   const int tid = ltid<NT>();
@@ -761,7 +788,12 @@ __global__ void __launch_bounds__(NT) svd_kernel(SvdArgs a) {
   constexpr int LD = 2 * CAP;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<CAP, NT> sm;
-  sm.carve(smem_raw, 0);
+  double2* gws = nullptr;
+  if constexpr (GlobalWs<CAP>::value)
+    gws = reinterpret_cast<double2*>(static_cast<double4*>(a.scratch) +
+                                     (int64_t)gridDim.x * LogW<CAP>::entries) +
+          (int64_t)blockIdx.x * GlobalWs<CAP>::complexes;
+  sm.carve(smem_raw, 0, gws);
   if constexpr (LogW<CAP>::value)
     sm.rlog = static_cast<double4*>(a.scratch) + (int64_t)blockIdx.x * LogW<CAP>::entries;
   const int tid = ltid<NT>();
@@ -841,7 +873,9 @@ int plan_grid(int64_t items, cudaStream_t st, int64_t* grid, void** scratch) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     *grid = items < sms ? items : sms;
-    cudaError_t e = cudaMallocAsync(scratch, sizeof(double4) * LogW<CAP>::entries * *grid, st);
+    size_t bytes = sizeof(double4) * LogW<CAP>::entries * *grid;
+    if constexpr (GlobalWs<CAP>::value) bytes += sizeof(double2) * GlobalWs<CAP>::complexes * *grid;
+    cudaError_t e = cudaMallocAsync(scratch, bytes, st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(rotation log)");
   }
   return MPSKQ_OK;
@@ -890,6 +924,9 @@ int launch_simulate(const SimArgs& a, void* stream) {
     case 24: return launch_sim_cap<24>(a, st);
     case 32: return launch_sim_cap<32>(a, st);
     case 48: return launch_sim_cap<48>(a, st);
+    case 64: return launch_sim_cap<64>(a, st);
+    case 80: return launch_sim_cap<80>(a, st);
+    case 96: return launch_sim_cap<96>(a, st);
   }
   return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", a.chi_cap);
 }
@@ -903,7 +940,10 @@ int launch_svd(const SvdArgs& a, void* stream) {
   if (big <= 32) return launch_svd_cap<16>(a, st);
   if (big <= 48) return launch_svd_cap<24>(a, st);
   if (big <= 64) return launch_svd_cap<32>(a, st);
-  return launch_svd_cap<48>(a, st);
+  if (big <= 96) return launch_svd_cap<48>(a, st);
+  if (big <= 128) return launch_svd_cap<64>(a, st);
+  if (big <= 160) return launch_svd_cap<80>(a, st);
+  return launch_svd_cap<96>(a, st);
 }
 
 // FP64 FMA throughput probe: 16 independent DFMA chains per thread

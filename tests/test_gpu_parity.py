@@ -340,15 +340,28 @@ def test_capacity_48_path_matches_reference():
         simulate_rows(g["X"], cfg, budget, chi_cap=32)
 
 
-def test_capacity_overflow_is_reported():
-    """config 5 at d=8 reaches chi 59 on these rows: beyond the largest
-    compiled capacity (48) the engine raises instead of truncating silently."""
+def test_large_chi_global_workspace_path():
+    """Config 5 at d=8 (m=100, budget 1e-16) peaks at chi 68 on these rows:
+    capacity 80 keeps theta in an L2-resident global workspace.  Bond dims
+    identical to the reference, K within the truncated tolerance."""
+    import time
+
     import paper_2411_09336_b200 as P
 
     g = golden("config5_m100_d8.npz")
     cfg, budget = _cfg(g)
-    with pytest.raises(RuntimeError, match="capacity"):
-        P.simulate_dataset(g["X"][:1], cfg, budget=budget)
+    t0 = time.time()
+    tr = P.simulate_dataset(g["X"], cfg, budget=budget)
+    te = P.simulate_dataset(g["X_test"], cfg, budget=budget)
+    print(f"d=8 simulation of 6 states: {time.time() - t0:.1f}s, capacity {tr.chi_cap}")
+    assert tr.chi_cap == 80
+    assert np.array_equal(tr.bond_dims(), g["train_chi"])
+    assert np.array_equal(te.bond_dims(), g["test_chi"])
+    assert np.array_equal(tr.peak.cpu().numpy(), g["train_peak"])
+    K = P.compute_gram(tr, tr, "train").entries
+    Kt = P.compute_gram(te, tr, "test").entries
+    assert np.abs(K - g["K_train"]).max() < 1e-6
+    assert np.abs(Kt - g["K_test"]).max() < 1e-6
 
 
 def test_svd_truncated_large_matrices():
