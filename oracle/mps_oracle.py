@@ -132,8 +132,13 @@ def gate_unitary(kind: str, angle) -> np.ndarray:
 
 
 # --------------------------------------------------------------------------- SVD
-def svd_truncated(mat: np.ndarray, budget: float):
-    """(U, s, Vh, discarded) of tensor.svd_truncated on a matrix (tensor.py:87-123)."""
+def svd_truncated(mat: np.ndarray, budget: float, chi_max: int = 0):
+    """(U, s, Vh, discarded) of tensor.svd_truncated on a matrix (tensor.py:87-123).
+
+    chi_max > 0 is an EXTENSION with no reference counterpart (BASELINE
+    config 2 names a chi_max): keep = min(keep, chi_max) after the budget
+    rule, the cut weight is discarded and renormalised like any other
+    (mps.py:189-192).  Unpinned by reference fixtures by construction."""
     if budget < 0:
         raise ValueError("budget must be non-negative")
     if not np.all(np.isfinite(mat)):
@@ -145,6 +150,8 @@ def svd_truncated(mat: np.ndarray, budget: float):
     tail = np.cumsum(sq[::-1])[::-1]
     cut = np.flatnonzero(tail <= budget)
     keep = max(int(cut[0]) if cut.size else s.size, 1)
+    if chi_max > 0:
+        keep = min(keep, chi_max)
     return u[:, :keep], s[:keep].copy(), vh[:keep], float(np.sum(sq[keep:]))
 
 
@@ -181,7 +188,7 @@ def _move_center(st: OracleState, target: int) -> None:
         st.center -= 1
 
 
-def simulate_gates(gates, m: int, budget: float, record_memory: bool = False) -> OracleState:
+def simulate_gates(gates, m: int, budget: float, record_memory: bool = False, chi_max: int = 0) -> OracleState:
     """simulate_circuit (mps.py:250-257) over a (kind, a, b, angle) list."""
     st = OracleState([np.array([1.0, 0.0], dtype=np.complex128).reshape(1, 2, 1) for _ in range(m)])
     two = [b >= 0 for _, _, b, _ in gates]
@@ -205,7 +212,7 @@ def simulate_gates(gates, m: int, budget: float, record_memory: bool = False) ->
             theta = np.tensordot(u.reshape(2, 2, 2, 2), theta, axes=((2, 3), (1, 2)))
             theta = theta.transpose(2, 0, 1, 3)
             cl, cr = theta.shape[0], theta.shape[3]
-            U, s, Vh, disc = svd_truncated(theta.reshape(cl * 2, 2 * cr), budget)
+            U, s, Vh, disc = svd_truncated(theta.reshape(cl * 2, 2 * cr), budget, chi_max)
             k = s.size
             if disc > 0.0:
                 kept = float(s @ s)
@@ -224,8 +231,8 @@ def simulate_gates(gates, m: int, budget: float, record_memory: bool = False) ->
     return st
 
 
-def simulate_row(x, m: int, r: int, d: int, gamma: float, budget: float) -> OracleState:
-    return simulate_gates(feature_map_gates(x, m, r, d, gamma), m, budget)
+def simulate_row(x, m: int, r: int, d: int, gamma: float, budget: float, chi_max: int = 0) -> OracleState:
+    return simulate_gates(feature_map_gates(x, m, r, d, gamma), m, budget, chi_max=chi_max)
 
 
 def overlap(bra_sites, ket_sites) -> complex:
