@@ -43,9 +43,21 @@ __device__ __forceinline__ double2 cfmac(double2 a, double2 b, double2 acc) {
 __device__ __forceinline__ double cnorm2(double2 a) { return fma(a.x, a.x, a.y * a.y); }
 __device__ __forceinline__ bool cfinite(double2 a) { return isfinite(a.x) && isfinite(a.y); }
 
+// A "thread group" of NT threads works on one state.  NT < 32: several
+// groups share a warp (aligned lane slices); NT == 32: one warp; NT > 32: a CTA.
+template <int NT>
+__device__ __forceinline__ unsigned group_mask() {
+  if constexpr (NT >= 32)
+    return kFull;
+  else
+    return ((1u << NT) - 1u) << ((threadIdx.x & 31) & ~(NT - 1));
+}
+
 template <int NT>
 __device__ __forceinline__ void bsync() {
-  if constexpr (NT == 32)
+  if constexpr (NT < 32)
+    __syncwarp(group_mask<NT>());
+  else if constexpr (NT == 32)
     __syncwarp();
   else
     __syncthreads();
@@ -53,35 +65,38 @@ __device__ __forceinline__ void bsync() {
 
 template <int NT>
 __device__ __forceinline__ int block_any(int v) {
-  if constexpr (NT == 32) {
-    __syncwarp();
-    return __any_sync(kFull, v);
+  if constexpr (NT <= 32) {
+    const unsigned m = group_mask<NT>();
+    __syncwarp(m);
+    return __any_sync(m, v);
   } else
     return __syncthreads_or(v);
 }
 
-// sum over aligned groups of G lanes (G a power of two <= 32); every lane of
-// the warp must call it.  The xor butterfly gives all lanes of a group the
+// sum over aligned groups of G lanes (G a power of two <= 32); every lane in
+// `mask` must call it.  The xor butterfly gives all lanes of a group the
 // bitwise-identical result.
-__device__ __forceinline__ double group_sum(double v, int G) {
-  for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+__device__ __forceinline__ double group_sum(double v, int G, unsigned mask = kFull) {
+  for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
   return v;
 }
-__device__ __forceinline__ double2 group_sum(double2 v, int G) {
+__device__ __forceinline__ double2 group_sum(double2 v, int G, unsigned mask = kFull) {
   for (int o = G >> 1; o > 0; o >>= 1) {
-    v.x += __shfl_xor_sync(kFull, v.x, o);
-    v.y += __shfl_xor_sync(kFull, v.y, o);
+    v.x += __shfl_xor_sync(mask, v.x, o);
+    v.y += __shfl_xor_sync(mask, v.y, o);
   }
   return v;
 }
 
-// CTA-wide sum, identical on every thread.  `red` needs NT/32 doubles.
+// sum over the thread group, identical on every thread.  `red` needs NT/32 doubles.
 template <int NT>
 __device__ __forceinline__ double block_sum(double v, double* red) {
-  v = group_sum(v, 32);
-  if constexpr (NT == 32) {
-    return v;
+  if constexpr (NT < 32) {
+    return group_sum(v, NT, group_mask<NT>());
+  } else if constexpr (NT == 32) {
+    return group_sum(v, 32);
   } else {
+    v = group_sum(v, 32);
     const int w = threadIdx.x >> 5;
     __syncthreads();
     if ((threadIdx.x & 31) == 0) red[w] = v;

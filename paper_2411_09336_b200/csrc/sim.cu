@@ -32,12 +32,13 @@ __device__ constexpr double kNoiseFloor = 10.0 * DBL_EPSILON;
 __device__ constexpr double kInvSqrt2 = 0.7071067811865475;
 constexpr int kMaxSweeps = 40;
 
-// thread index within the state's thread group: NT == 32 kernels carry one
-// state per warp (several lockstepped warps per CTA), larger NT one per CTA
+// thread index within the state's thread group: NT <= 32 kernels carry one
+// state per NT-lane slice of a warp (several lockstepped groups per CTA),
+// larger NT one state per CTA
 template <int NT>
 __device__ __forceinline__ int ltid() {
-  if constexpr (NT == 32)
-    return threadIdx.x & 31;
+  if constexpr (NT <= 32)
+    return threadIdx.x & (NT - 1);
   else
     return threadIdx.x;
 }
@@ -45,7 +46,7 @@ __device__ __forceinline__ int ltid() {
 template <int CAP>
 struct NtFor {
   static constexpr int value =
-      CAP <= 4 ? 32 : CAP <= 8 ? 64 : CAP <= 16 ? 128 : CAP <= 32 ? 256 : CAP <= 48 ? 384 : 512;
+      CAP <= 4 ? 16 : CAP <= 8 ? 64 : CAP <= 16 ? 128 : CAP <= 32 ? 256 : CAP <= 48 ? 384 : 512;
 };
 
 // Capacities above 48: theta/C and the staging buffer no longer fit shared
@@ -153,7 +154,7 @@ __device__ void apply_reflector(double2* M, const double2* u, double tau, int j,
     if (act)
       #pragma unroll 1
       for (int r = j + g; r < Rr; r += G) acc = cfmac(u[r], M[c * LD + r], acc);
-    acc = group_sum(acc, G);
+    acc = group_sum(acc, G, group_mask<NT>());
     if (act) {
       const double2 w = cscale(acc, tau);
       #pragma unroll 1
@@ -218,9 +219,9 @@ __device__ __forceinline__ double2 r_entry(const Smem<CAP, NT>& sm, int kk, int 
 // Column pairs follow the circle-method round robin (n/2 disjoint pairs per
 // round, ne-1 rounds per sweep), one group of G lanes per pair.
 template <int G>
-__device__ __forceinline__ double gsum(double v) {
+__device__ __forceinline__ double gsum(double v, unsigned mask) {
 #pragma unroll
-  for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
   return v;
 }
 
@@ -259,6 +260,7 @@ __device__ __noinline__ int jacobi_sweeps(Smem<CAP, NT>& sm, int Rr, int n) {
   const double tol = DBL_EPSILON * (double)max(Rr, 8);
   const double tol2 = tol * tol;
   const int max_rounds = kMaxSweeps * span;
+  const unsigned msk = group_mask<NT>();
   int round = 0, quiet = 0;
   for (; round < max_rounds;) {
     const int t = round % span;
@@ -276,10 +278,10 @@ __device__ __noinline__ int jacobi_sweeps(Smem<CAP, NT>& sm, int Rr, int n) {
         gy = fma(x.x, y.y, fma(-x.y, y.x, gy));
       }
     }
-    a = gsum<G>(a);
-    b = gsum<G>(b);
-    gx = gsum<G>(gx);
-    gy = gsum<G>(gy);
+    a = gsum<G>(a, msk);
+    b = gsum<G>(b, msk);
+    gx = gsum<G>(gx, msk);
+    gy = gsum<G>(gy, msk);
     const double g2 = fma(gx, gx, gy * gy);
     const bool rot = act && g2 > tol2 * a * b && g2 > 0.0;
     double4* entry = nullptr;
@@ -400,7 +402,7 @@ __device__ __noinline__ void norms_and_order(Smem<CAP, NT>& sm, int Rr, int n) {
     if (c < n)
       #pragma unroll 1
       for (int r = g; r < Rr; r += G) acc += cnorm2(sm.A[c * LD + r]);
-    acc = group_sum(acc, G);
+    acc = group_sum(acc, G, group_mask<NT>());
     if (c < n && g == 0) sm.sig[c] = sqrt(acc);
   }
   bsync<NT>();
@@ -701,14 +703,14 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
 // region of the (large) op code and the instruction cache keeps up.
 template <int NT>
 struct SpcFor {
-  static constexpr int value = NT == 32 ? 4 : 1;
+  static constexpr int value = NT <= 32 ? 128 / NT : 1;
 };
 
 template <int CAP, int NT>
 __global__ void __launch_bounds__(NT * SpcFor<NT>::value) sim_kernel(SimArgs a) {
   constexpr int SPC = SpcFor<NT>::value;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int slot = SPC > 1 ? (int)(threadIdx.x >> 5) : 0;
+  const int slot = SPC > 1 ? (int)(threadIdx.x / NT) : 0;
   Smem<CAP, NT> sm;
   double2* gws = nullptr;
   if constexpr (GlobalWs<CAP>::value)
