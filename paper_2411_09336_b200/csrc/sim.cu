@@ -370,7 +370,8 @@ __device__ int jacobi(Smem<CAP, NT>& sm, int Rr, int n) {
   if (G >= 32) return jacobi_sweeps<CAP, NT, 32>(sm, Rr, n);
   if (G == 16) return jacobi_sweeps<CAP, NT, 16>(sm, Rr, n);
   if (G == 8) return jacobi_sweeps<CAP, NT, 8>(sm, Rr, n);
-  return jacobi_sweeps<CAP, NT, 4>(sm, Rr, n);
+  if (G == 4) return jacobi_sweeps<CAP, NT, 4>(sm, Rr, n);
+  return jacobi_sweeps<CAP, NT, 2>(sm, Rr, n);
 }
 
 // log mode: rebuild W (n x n) in Wm from the rotation log
@@ -385,8 +386,10 @@ __device__ void replay(Smem<CAP, NT>& sm, double2* Wm, int n, int sweeps) {
     replay_sweeps<CAP, NT, 16>(sm, Wm, n, sweeps);
   else if (G == 8)
     replay_sweeps<CAP, NT, 8>(sm, Wm, n, sweeps);
-  else
+  else if (G == 4)
     replay_sweeps<CAP, NT, 4>(sm, Wm, n, sweeps);
+  else
+    replay_sweeps<CAP, NT, 2>(sm, Wm, n, sweeps);
 }
 
 // column norms of C, descending order in perm (ties keep index order)
