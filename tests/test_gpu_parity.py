@@ -378,3 +378,37 @@ def test_svd_truncated_large_matrices():
         k = s.size
         assert np.abs(U.conj().T @ U - np.eye(k)).max() < 1e-11
         assert np.abs(Vh @ Vh.conj().T - np.eye(k)).max() < 1e-11
+
+
+def test_integration_md_ctypes_stub_runs():
+    """The binding a maintainer would add to the reference
+    works as written: exec it against the golden config-1 rows."""
+    import re
+    from dataclasses import dataclass
+
+    from conftest import ROOT
+
+    import paper_2411_09336_b200 as P
+
+    text = (ROOT / "INTEGRATION.md").read_text()
+    block = re.search(r"```python\n(import ctypes.*?)```", text, re.S).group(1)
+    block = block.replace('"/path/to/paper_2411_09336_b200/libmpskq.so"',
+                          repr(str(ROOT / "paper_2411_09336_b200" / "libmpskq.so")))
+
+    @dataclass
+    class GramMatrix:
+        entries: np.ndarray
+        kind: str
+
+    ns = {"GramMatrix": GramMatrix, "DEFAULT_TRUNC_BUDGET": 1e-24}
+    exec(block, ns)
+    g = golden("config1_m8_d1.npz")
+    cfg, budget = _cfg(g)
+    rep = P.RunReport()
+    K = ns["run_distributed"](g["X"], g["X"], cfg, P.make_schedule(64, 64, 1, "round_robin", "train"),
+                              budget=budget, report=rep).entries
+    assert np.abs(K - g["K_train"]).max() < 1e-10
+    Kt = ns["run_distributed"](g["X_test"], g["X"], cfg, P.make_schedule(16, 64, 1, "round_robin", "test"),
+                               budget=budget).entries
+    assert np.abs(Kt - g["K_test"]).max() < 1e-10
+    assert rep.n_inner_products == 64 * 63 // 2
