@@ -12,7 +12,8 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libmpskq.so"
+# MPSKQ_LIB overrides the in-tree library (A/B experiments only)
+LIB_PATH = Path(os.environ.get("MPSKQ_LIB") or Path(__file__).resolve().parent / "libmpskq.so")
 
 OK = 0
 ERR_INVALID = -1
