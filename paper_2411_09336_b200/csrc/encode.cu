@@ -40,6 +40,7 @@ __global__ void encode_kernel(const double* __restrict__ X, int64_t n_rows, int 
 int launch_encode(const double* X, int64_t n_rows, int m, int r, int d, double gamma, double* coef,
                   int* bad, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  retain_pool_memory();
   // interaction_graph (ansatz.py:102-106) uploaded once per call (tiny)
   int E = 0;
   for (int k = 1; k <= d; ++k) E += m - k;

@@ -22,6 +22,11 @@ inline bool chi_cap_supported(int c) {
   return false;
 }
 
+// Keep the device's stream-ordered pool pages between calls (the default
+// release threshold 0 hands them back to the driver at every synchronisation,
+// and re-mapping a GB of workspace costs tens of ms).  Idempotent, cheap.
+void retain_pool_memory();
+
 // layout helper (also used on device through the site_off table)
 int64_t bond_cap(int m, int chi_cap, int b);
 

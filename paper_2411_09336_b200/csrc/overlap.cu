@@ -24,6 +24,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "device.cuh"
 #include "internal.h"
 
@@ -40,7 +42,8 @@ constexpr int kWarpsO1 = 8;            // bras per CTA tile
 // sim layout -> [site][block][entry][lane] (double2), zero padded to 4x2x4
 __global__ void pack_o1_kernel(const double2* __restrict__ sites, const int32_t* __restrict__ chi,
                                const int64_t* __restrict__ site_off, int64_t stride, int m,
-                               int64_t n, int64_t nblk, double2* __restrict__ out) {
+                               int64_t n, int64_t nblk, const int32_t* __restrict__ perm,
+                               double2* __restrict__ out) {
   const int64_t total = (int64_t)m * nblk * kEnt * kLanes;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -48,14 +51,48 @@ __global__ void pack_o1_kernel(const double2* __restrict__ sites, const int32_t*
     const int e = (int)((idx / kLanes) % kEnt);
     const int64_t blk = (idx / (kLanes * kEnt)) % nblk;
     const int s = (int)(idx / ((int64_t)kLanes * kEnt * nblk));
-    const int64_t state = blk * kLanes + lane;
+    const int64_t pos = blk * kLanes + lane;
     double2 v = make_double2(0.0, 0.0);
-    if (state < n) {
+    if (pos < n) {
+      const int64_t state = perm ? perm[pos] : pos;
       const int k = e / (2 * kP), p = (e / kP) & 1, r = e % kP;
       const int chl = chi[state * (m + 1) + s], chr = chi[state * (m + 1) + s + 1];
       if (k < chl && r < chr) v = sites[state * stride + site_off[s] + (k * 2 + p) * chr + r];
     }
     out[idx] = v;
+  }
+}
+
+// Ket ordering key: one bit per window of bonds that holds a chi = 4 bond,
+// most significant first, so sorting groups kets whose wide bonds coincide
+// and 32-ket blocks more often have max chi <= 3 at a bond.
+__global__ void ket_key_kernel(const int32_t* __restrict__ chi, int m, int64_t n,
+                               uint32_t* __restrict__ keys, int32_t* __restrict__ vals) {
+  const int win = (m + 1 + 31) / 32;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t key = 0;
+    for (int b = 0; b <= m; ++b)
+      if (chi[idx * (m + 1) + b] >= kP) key |= 1u << (31 - b / win);
+    keys[idx] = key;
+    vals[idx] = (int32_t)idx;
+  }
+}
+
+// per block of 32 (ordered) kets and bond: 1 if every ket has chi <= 3 there
+__global__ void block_narrow_kernel(const int32_t* __restrict__ chi, const int32_t* __restrict__ perm,
+                                    int m, int64_t n, int64_t nblk, uint8_t* __restrict__ out) {
+  const int64_t total = nblk * (m + 1);
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t blk = idx / (m + 1);
+    const int b = (int)(idx % (m + 1));
+    int mx = 1;
+    for (int l = 0; l < kLanes; ++l) {
+      const int64_t pos = blk * kLanes + l;
+      if (pos < n) mx = max(mx, chi[(perm ? perm[pos] : pos) * (m + 1) + b]);
+    }
+    out[idx] = mx < kP;
   }
 }
 
@@ -77,15 +114,17 @@ __device__ __forceinline__ void store_result(int out_mode, double* out, int64_t 
 // 8 bras of a tile at one site are one contiguous 4 KB run for a bulk copy
 __global__ void pack_bra_kernel(const double2* __restrict__ sites, const int32_t* __restrict__ chi,
                                 const int64_t* __restrict__ site_off, int64_t stride, int m,
-                                int64_t n, int64_t n_pad, double2* __restrict__ out) {
+                                int64_t n, int64_t n_pad, const int32_t* __restrict__ perm,
+                                double2* __restrict__ out) {
   const int64_t total = (int64_t)m * n_pad * kEnt;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int e = (int)(idx % kEnt);
-    const int64_t state = (idx / kEnt) % n_pad;
+    const int64_t pos = (idx / kEnt) % n_pad;
     const int s = (int)(idx / ((int64_t)kEnt * n_pad));
     double2 v = make_double2(0.0, 0.0);
-    if (state < n) {
+    if (pos < n) {
+      const int64_t state = perm ? perm[pos] : pos;
       const int k = e / (2 * kP), p = (e / kP) & 1, r = e % kP;
       const int chl = chi[state * (m + 1) + s], chr = chi[state * (m + 1) + s + 1];
       if (k < chl && r < chr) v = sites[state * stride + site_off[s] + (k * 2 + p) * chr + r];
@@ -108,10 +147,13 @@ struct O1Args {
   const int32_t* bra_chi;
   int64_t n_bras, n_kets, n_pad_bra, nblk_ket;
   int m, kind, out_mode;
-  const int2* tiles;  // (bra tile of 8, ket block of 32)
+  const int2* tiles;  // (bra tile of 8, ket block of 32), in ordered positions
   int64_t n_tiles;
   double* out;
   int64_t ld;
+  const int32_t* bperm;      // ordered position -> bra index (nullable)
+  const int32_t* kperm;      // ordered position -> ket index
+  const uint8_t* kb_narrow;  // [ket block][bond]: block max chi <= 3
 };
 
 // Site step of one (bra, ket) pair, in two halves with many independent
@@ -125,7 +167,7 @@ struct O1Args {
 // The bra's bond dims are exact (warp-uniform); kb/br run over the zero-padded
 // 4 because the 32 kets of a warp rarely share a smaller bound.
 template <int NA>
-__device__ __forceinline__ void o1_phase1(const double2 (&env)[kP][kP], const double2* B,
+__device__ __forceinline__ void o1_phase1(const double2 (&env)[kP][kP], const double2* B, bool narrow,
                                           double2 (&T)[kP][2][kP]) {
 #pragma unroll
   for (int al = 0; al < NA; ++al)
@@ -135,6 +177,7 @@ __device__ __forceinline__ void o1_phase1(const double2 (&env)[kP][kP], const do
       for (int br = 0; br < kP; ++br) T[al][p][br] = make_double2(0.0, 0.0);
 #pragma unroll
   for (int kb = 0; kb < kP; ++kb) {
+    if (kb == kP - 1 && narrow) break;  // every ket of the block has chi_s <= 3
     double2 b[2][kP];
 #pragma unroll
     for (int p = 0; p < 2; ++p)
@@ -273,7 +316,9 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
     const int64_t i = (int64_t)tile.x * kWarpsO1 + warp;  // bra (warp-uniform)
     const int64_t j = (int64_t)tile.y * kLanes + lane;    // ket (per lane)
     const int64_t ic = i < a.n_bras ? i : a.n_bras - 1;
-    for (int b = lane; b <= m; b += kLanes) mychi[b] = __ldg(a.bra_chi + ic * (m + 1) + b);
+    const int64_t ib = a.bperm ? a.bperm[ic] : ic;  // bra index of this warp
+    const uint8_t* narrow = a.kb_narrow + (int64_t)tile.y * (m + 1);
+    for (int b = lane; b <= m; b += kLanes) mychi[b] = __ldg(a.bra_chi + ib * (m + 1) + b);
     __syncwarp();
     double2 env[kP][kP];
 #pragma unroll
@@ -291,11 +336,12 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
       const double2* B = sket + buf * kEnt * kLanes + lane;  // B[e] at B[e * 32]
       const double2* A = sbra + buf * kWarpsO1 * kEnt + warp * kEnt;
       double2 T[kP][2][kP];
+      const bool nar = __ldg(narrow + s) != 0;
       switch (na) {
-        case 1: o1_phase1<1>(env, B, T); break;
-        case 2: o1_phase1<2>(env, B, T); break;
-        case 3: o1_phase1<3>(env, B, T); break;
-        default: o1_phase1<4>(env, B, T); break;
+        case 1: o1_phase1<1>(env, B, nar, T); break;
+        case 2: o1_phase1<2>(env, B, nar, T); break;
+        case 3: o1_phase1<3>(env, B, nar, T); break;
+        default: o1_phase1<4>(env, B, nar, T); break;
       }
       o1_phase2(A, T, na, na1, env);
       __syncwarp();
@@ -304,8 +350,8 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
       na = na1;
     }
     const bool train = a.kind == MPSKQ_KIND_TRAIN;
-    const bool valid = i < a.n_bras && j < a.n_kets && (!train || i < j);
-    if (valid) store_result(a.out_mode, a.out, a.ld, i, j, env[0][0], train);
+    const bool valid = i < a.n_bras && j < a.n_kets && (!train || i < j);  // ordered positions
+    if (valid) store_result(a.out_mode, a.out, a.ld, ib, a.kperm[j], env[0][0], train);
     __syncwarp();
   }
 }
@@ -526,36 +572,79 @@ std::vector<int2> make_tiles(bool train, int64_t n_rows, int64_t n_cols, int rb,
 
 int launch_o1(const OverlapArgs& a, cudaStream_t st) {
   const int m = a.m;
+  const bool train = a.kind == MPSKQ_KIND_TRAIN;
   const int64_t npb = (a.n_bras + kWarpsO1 - 1) / kWarpsO1 * kWarpsO1;
   const int64_t nbk = (a.n_kets + kLanes - 1) / kLanes;
   const size_t bb = sizeof(double2) * (size_t)m * npb * kEnt;
   const size_t kb = sizeof(double2) * (size_t)m * nbk * kEnt * kLanes;
-  void *bra = nullptr, *ket = nullptr;
-  cudaError_t e = cudaMallocAsync(&bra, bb, st);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(packed bras)");
-  e = cudaMallocAsync(&ket, kb, st);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(packed kets)");
   const int threads = 256;
   auto blocks_for = [&](int64_t total) {
     return (int)std::min<int64_t>((total + threads - 1) / threads, 148 * 64);
   };
+  std::vector<void*> frees;
+  auto alloc = [&](void** p, size_t bytes, const char* what) {
+    cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 8, st);
+    if (e != cudaSuccess) return cuda_fail(e, what);
+    frees.push_back(*p);
+    return (int)MPSKQ_OK;
+  };
+  auto release = [&]() {
+    for (void* p : frees) cudaFreeAsync(p, st);
+  };
+  // order the kets (train: both sides share the order, so i < j stays a triangle)
+  void *keys = nullptr, *keys2 = nullptr, *vals = nullptr, *perm = nullptr, *narrow = nullptr, *tmp = nullptr;
+  int s_ = MPSKQ_OK;
+  if ((s_ = alloc(&keys, sizeof(uint32_t) * a.n_kets, "keys")) || (s_ = alloc(&keys2, sizeof(uint32_t) * a.n_kets, "keys")) ||
+      (s_ = alloc(&vals, sizeof(int32_t) * a.n_kets, "vals")) || (s_ = alloc(&perm, sizeof(int32_t) * a.n_kets, "perm")) ||
+      (s_ = alloc(&narrow, (size_t)nbk * (m + 1), "narrow"))) {
+    release();
+    return s_;
+  }
+  ket_key_kernel<<<blocks_for(a.n_kets), threads, 0, st>>>(a.ket_chi, m, a.n_kets, static_cast<uint32_t*>(keys),
+                                                           static_cast<int32_t*>(vals));
+  size_t tmp_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, static_cast<uint32_t*>(keys), static_cast<uint32_t*>(keys2),
+                                  static_cast<int32_t*>(vals), static_cast<int32_t*>(perm), (int)a.n_kets, 0, 32, st);
+  if ((s_ = alloc(&tmp, tmp_bytes, "sort scratch"))) {
+    release();
+    return s_;
+  }
+  cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, static_cast<uint32_t*>(keys), static_cast<uint32_t*>(keys2),
+                                  static_cast<int32_t*>(vals), static_cast<int32_t*>(perm), (int)a.n_kets, 0, 32, st);
+  const int32_t* kperm = static_cast<const int32_t*>(perm);
+  const int32_t* bperm = train ? kperm : nullptr;
+  block_narrow_kernel<<<blocks_for(nbk * (m + 1)), threads, 0, st>>>(a.ket_chi, kperm, m, a.n_kets, nbk,
+                                                                    static_cast<uint8_t*>(narrow));
+  void *bra = nullptr, *ket = nullptr;
+  if ((s_ = alloc(&bra, bb, "packed bras")) || (s_ = alloc(&ket, kb, "packed kets"))) {
+    release();
+    return s_;
+  }
   pack_bra_kernel<<<blocks_for((int64_t)m * npb * kEnt), threads, 0, st>>>(
       reinterpret_cast<const double2*>(a.bra_sites), a.bra_chi, a.site_off, a.state_stride, m,
-      a.n_bras, npb, static_cast<double2*>(bra));
+      a.n_bras, npb, bperm, static_cast<double2*>(bra));
   pack_o1_kernel<<<blocks_for((int64_t)m * nbk * kEnt * kLanes), threads, 0, st>>>(
       reinterpret_cast<const double2*>(a.ket_sites), a.ket_chi, a.site_off, a.state_stride, m,
-      a.n_kets, nbk, static_cast<double2*>(ket));
-  const bool train = a.kind == MPSKQ_KIND_TRAIN;
+      a.n_kets, nbk, kperm, static_cast<double2*>(ket));
   auto tiles = make_tiles(train, a.n_bras, a.n_kets, kWarpsO1, kLanes, a.rank, a.world);
   int2* dtiles = nullptr;
-  if (int s = upload_tiles(tiles, &dtiles, st)) return s;
+  if ((s_ = upload_tiles(tiles, &dtiles, st))) {
+    release();
+    return s_;
+  }
+  frees.push_back(dtiles);
+  cudaError_t e = cudaSuccess;
   if (!tiles.empty()) {
     const size_t smem = o1_smem_bytes(m);
     e = cudaFuncSetAttribute(overlap_o1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(o1)");
+    if (e != cudaSuccess) {
+      release();
+      return cuda_fail(e, "cudaFuncSetAttribute(o1)");
+    }
     O1Args o{static_cast<const double2*>(bra), static_cast<const double2*>(ket), a.bra_chi,
              a.n_bras, a.n_kets, npb, nbk, m, a.kind,
-             a.out_mode, dtiles, (int64_t)tiles.size(), a.out, a.ld};
+             a.out_mode, dtiles, (int64_t)tiles.size(), a.out, a.ld,
+             bperm, kperm, static_cast<const uint8_t*>(narrow)};
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -564,10 +653,8 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
     overlap_o1_kernel<<<grid, kWarpsO1 * 32, smem, st>>>(o);
   }
   e = cudaGetLastError();
+  release();
   if (e != cudaSuccess) return cuda_fail(e, "overlap_o1 launch");
-  cudaFreeAsync(dtiles, st);
-  cudaFreeAsync(ket, st);
-  cudaFreeAsync(bra, st);
   return MPSKQ_OK;
 }
 
@@ -623,6 +710,7 @@ int launch_mma(const OverlapArgs& a, cudaStream_t st) {
 
 int launch_overlap(const OverlapArgs& a, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  retain_pool_memory();
   int s = MPSKQ_OK;
   switch (a.chi_cap) {
     case 4: s = launch_o1(a, st); break;

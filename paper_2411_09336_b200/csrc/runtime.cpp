@@ -33,6 +33,19 @@ int cuda_fail(int err, const char* what) {
   return fail(MPSKQ_ERR_CUDA, "%s: %s", what, cudaGetErrorString((cudaError_t)err));
 }
 
+void retain_pool_memory() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  static thread_local int done_for = -1;
+  if (done_for == dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_for = dev;
+}
+
 int64_t bond_cap(int m, int chi_cap, int b) {
   int e = std::min(b, m - b);
   if (e >= 30) return chi_cap;

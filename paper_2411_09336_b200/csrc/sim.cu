@@ -921,6 +921,7 @@ int launch_svd_cap(const SvdArgs& a0, cudaStream_t st) {
 
 int launch_simulate(const SimArgs& a, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  retain_pool_memory();
   switch (a.chi_cap) {
     case 4: return launch_sim_cap<4>(a, st);
     case 8: return launch_sim_cap<8>(a, st);
@@ -938,6 +939,7 @@ int launch_simulate(const SimArgs& a, void* stream) {
 
 int launch_svd(const SvdArgs& a, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  retain_pool_memory();
   const int big = a.rows > a.cols ? a.rows : a.cols;
   if (big <= 8) return launch_svd_cap<4>(a, st);
   if (big <= 16) return launch_svd_cap<8>(a, st);
