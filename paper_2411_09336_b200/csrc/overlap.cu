@@ -96,6 +96,22 @@ __global__ void block_narrow_kernel(const int32_t* __restrict__ chi, const int32
   }
 }
 
+__global__ void invert_perm_kernel(const int32_t* __restrict__ perm, int64_t n, int32_t* __restrict__ inv) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
+    inv[perm[p]] = (int32_t)p;
+}
+
+// out[a][b] = ordered[bpos[a]][kpos[b]] (row gather, coalesced writes).  For
+// the train kind `ordered` holds both triangles; the diagonal is filled later.
+template <class T>
+__global__ void unpermute_kernel(const T* __restrict__ ordered, int64_t nk, const int32_t* __restrict__ bpos,
+                                 const int32_t* __restrict__ kpos, int64_t nb, T* __restrict__ out, int64_t ld) {
+  for (int64_t a = blockIdx.x; a < nb; a += gridDim.x) {
+    const T* row = ordered + (int64_t)(bpos ? bpos[a] : a) * nk;
+    for (int64_t b = threadIdx.x; b < nk; b += blockDim.x) out[a * ld + b] = row[kpos[b]];
+  }
+}
+
 __device__ __forceinline__ void store_result(int out_mode, double* out, int64_t ld, int64_t i,
                                              int64_t j, double2 ov, bool mirror) {
   if (out_mode == MPSKQ_OUT_KERNEL) {
@@ -350,8 +366,10 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
       na = na1;
     }
     const bool train = a.kind == MPSKQ_KIND_TRAIN;
-    const bool valid = i < a.n_bras && j < a.n_kets && (!train || i < j);  // ordered positions
-    if (valid) store_result(a.out_mode, a.out, a.ld, ib, a.kperm[j], env[0][0], train);
+    // results go to the ordered index space (full-sector tile rows); a gather
+    // pass maps them back to the callers' indices
+    const bool valid = i < a.n_bras && j < a.n_kets && (!train || i < j);
+    if (valid) store_result(a.out_mode, a.out, a.ld, i, j, env[0][0], train);
     __syncwarp();
   }
 }
@@ -613,6 +631,15 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
                                   static_cast<int32_t*>(vals), static_cast<int32_t*>(perm), (int)a.n_kets, 0, 32, st);
   const int32_t* kperm = static_cast<const int32_t*>(perm);
   const int32_t* bperm = train ? kperm : nullptr;
+  void *kinv = nullptr, *ordered = nullptr;
+  const size_t elem = a.out_mode == MPSKQ_OUT_KERNEL ? sizeof(double) : sizeof(double2);
+  if ((s_ = alloc(&kinv, sizeof(int32_t) * a.n_kets, "inverse perm")) ||
+      (s_ = alloc(&ordered, elem * (size_t)a.n_bras * a.n_kets, "ordered results"))) {
+    release();
+    return s_;
+  }
+  invert_perm_kernel<<<blocks_for(a.n_kets), threads, 0, st>>>(kperm, a.n_kets, static_cast<int32_t*>(kinv));
+  if (a.world > 1) cudaMemsetAsync(ordered, 0, elem * (size_t)a.n_bras * a.n_kets, st);
   block_narrow_kernel<<<blocks_for(nbk * (m + 1)), threads, 0, st>>>(a.ket_chi, kperm, m, a.n_kets, nbk,
                                                                     static_cast<uint8_t*>(narrow));
   void *bra = nullptr, *ket = nullptr;
@@ -643,7 +670,7 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
     }
     O1Args o{static_cast<const double2*>(bra), static_cast<const double2*>(ket), a.bra_chi,
              a.n_bras, a.n_kets, npb, nbk, m, a.kind,
-             a.out_mode, dtiles, (int64_t)tiles.size(), a.out, a.ld,
+             a.out_mode, dtiles, (int64_t)tiles.size(), static_cast<double*>(ordered), a.n_kets,
              bperm, kperm, static_cast<const uint8_t*>(narrow)};
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -651,6 +678,15 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
     // persistent: one CTA per SM walks the tile list (the ring stays warm)
     const int grid = (int)std::min<int64_t>((int64_t)tiles.size(), sms);
     overlap_o1_kernel<<<grid, kWarpsO1 * 32, smem, st>>>(o);
+    const int32_t* bpos = train ? static_cast<const int32_t*>(kinv) : nullptr;
+    const int rows = (int)std::min<int64_t>(a.n_bras, 148 * 32);
+    if (a.out_mode == MPSKQ_OUT_KERNEL)
+      unpermute_kernel<double><<<rows, 256, 0, st>>>(static_cast<const double*>(ordered), a.n_kets, bpos,
+                                                     static_cast<const int32_t*>(kinv), a.n_bras, a.out, a.ld);
+    else
+      unpermute_kernel<double2><<<rows, 256, 0, st>>>(static_cast<const double2*>(ordered), a.n_kets, bpos,
+                                                       static_cast<const int32_t*>(kinv), a.n_bras,
+                                                       reinterpret_cast<double2*>(a.out), a.ld);
   }
   e = cudaGetLastError();
   release();
