@@ -60,7 +60,9 @@ struct GlobalWs {
 
 // Capacities above 32 keep only theta/C in shared memory: the Jacobi rotations
 // are logged to a per-CTA global buffer and replayed on the identity after
-// the C-side factor has been written out (W then reuses C's space).
+// the C-side factor has been written out (W then reuses C's space).  (Using it
+// from capacity 12 up doubles the resident states but the replay costs about
+// as much as it saves: measured neutral to negative.)
 template <int CAP>
 struct LogW {
   static constexpr bool value = CAP > 32;
@@ -869,15 +871,20 @@ int prepare(K kernel, size_t smem) {
 }
 
 // grid and rotation-log scratch; capacities > 32 run one persistent CTA per SM
-template <int CAP>
-int plan_grid(int64_t items, cudaStream_t st, int64_t* grid, void** scratch) {
+template <int CAP, class K>
+int plan_grid(K kernel, int threads, size_t smem, int64_t items, cudaStream_t st, int64_t* grid, void** scratch) {
   *grid = items < (int64_t(1) << 30) ? items : (int64_t(1) << 30);
   *scratch = nullptr;
   if constexpr (LogW<CAP>::value) {
-    int dev = 0, sms = 148;
+    // persistent grid of all co-resident CTAs, each with its own log slice
+    int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    *grid = items < sms ? items : sms;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    const int64_t cap = (int64_t)sms * per_sm;
+    *grid = items < cap ? items : cap;
     size_t bytes = sizeof(double4) * LogW<CAP>::entries * *grid;
     if constexpr (GlobalWs<CAP>::value) bytes += sizeof(double2) * GlobalWs<CAP>::complexes * *grid;
     cudaError_t e = cudaMallocAsync(scratch, bytes, st);
@@ -894,7 +901,9 @@ int launch_sim_cap(const SimArgs& a0, cudaStream_t st) {
   if (int s = prepare(sim_kernel<CAP, NT>, smem)) return s;
   SimArgs a = a0;
   int64_t grid = 0;
-  if (int s = plan_grid<CAP>((a.n_states + SPC - 1) / SPC, st, &grid, &a.scratch)) return s;
+  if (int s = plan_grid<CAP>(sim_kernel<CAP, NT>, NT * SPC, smem, (a.n_states + SPC - 1) / SPC, st, &grid,
+                             &a.scratch))
+    return s;
   sim_kernel<CAP, NT><<<(unsigned)grid, NT * SPC, smem, st>>>(a);
   cudaError_t e = cudaGetLastError();
   if (a.scratch) cudaFreeAsync(a.scratch, st);
@@ -909,7 +918,7 @@ int launch_svd_cap(const SvdArgs& a0, cudaStream_t st) {
   if (int s = prepare(svd_kernel<CAP, NT>, smem)) return s;
   SvdArgs a = a0;
   int64_t grid = 0;
-  if (int s = plan_grid<CAP>(a.batch, st, &grid, &a.scratch)) return s;
+  if (int s = plan_grid<CAP>(svd_kernel<CAP, NT>, NT, smem, a.batch, st, &grid, &a.scratch)) return s;
   svd_kernel<CAP, NT><<<(unsigned)grid, NT, smem, st>>>(a);
   cudaError_t e = cudaGetLastError();
   if (a.scratch) cudaFreeAsync(a.scratch, st);
