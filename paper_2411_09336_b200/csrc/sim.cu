@@ -32,6 +32,11 @@ __device__ constexpr double kNoiseFloor = 10.0 * DBL_EPSILON;
 __device__ constexpr double kInvSqrt2 = 0.7071067811865475;
 constexpr int kMaxSweeps = 40;
 
+#ifdef MPSKQ_DEBUG_COUNTERS
+// debug builds only: Jacobi rounds and two-qubit SVDs, summed over states
+__device__ unsigned long long g_dbg_rounds = 0, g_dbg_svds = 0, g_dbg_span = 0;
+#endif
+
 // thread index within the state's thread group: NT <= 32 kernels carry one
 // state per NT-lane slice of a warp (several lockstepped groups per CTA),
 // larger NT one state per CTA
@@ -263,6 +268,20 @@ __device__ __noinline__ int jacobi_sweeps(Smem<CAP, NT>& sm, int Rr, int n) {
   const double tol2 = tol * tol;
   const int max_rounds = kMaxSweeps * span;
   const unsigned msk = group_mask<NT>();
+  // Pairs with a column below half the truncation noise floor are left alone:
+  // such columns are zeroed by the floor (10 eps s0, tensor.py:108-109) and
+  // cannot combine across it, and their coupling moves a kept sigma^2 by at
+  // most |c_small|^2 <= (5 eps s0)^2 -- far below the LAPACK-vs-Jacobi
+  // rounding already present -- but rotating on their rounding noise was what
+  // kept large thetas sweeping (measured 12-15 sweeps at chi 17-44).
+  // ||theta||_F^2 / 4 * eps^2 <= (5 eps s0)^2 for n <= 100 columns.
+  double fro = 0.0;
+  #pragma unroll 1
+  for (int idx = tid; idx < Rr * n; idx += NT) {
+    const int c = idx / Rr, r = idx - c * Rr;
+    fro += cnorm2(A[c * LD + r]);
+  }
+  const double noise2 = 0.25 * DBL_EPSILON * DBL_EPSILON * block_sum<NT>(fro, sm.red);
   int round = 0, quiet = 0;
   for (; round < max_rounds;) {
     const int t = round % span;
@@ -285,7 +304,7 @@ __device__ __noinline__ int jacobi_sweeps(Smem<CAP, NT>& sm, int Rr, int n) {
     gx = gsum<G>(gx, msk);
     gy = gsum<G>(gy, msk);
     const double g2 = fma(gx, gx, gy * gy);
-    const bool rot = act && g2 > tol2 * a * b && g2 > 0.0;
+    const bool rot = act && g2 > tol2 * a * b && g2 > 0.0 && fmin(a, b) > noise2;
     double4* entry = nullptr;
     if constexpr (kLog) entry = sm.rlog + (int64_t)round * P + k;
     if (kLog && act && g == 0 && !rot) *entry = make_double4(1.0, 0.0, 0.0, 0.0);
@@ -647,6 +666,13 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
   const int n = left ? Nc : Mr;
   const int kmin = min(Mr, Nc);
   const int sweeps = jacobi<CAP, NT>(sm, Rr, n);
+#ifdef MPSKQ_DEBUG_COUNTERS
+  if (tid == 0) {
+    atomicAdd(&g_dbg_rounds, (unsigned long long)sweeps);
+    atomicAdd(&g_dbg_svds, 1ull);
+    atomicAdd(&g_dbg_span, (unsigned long long)(n + (n & 1) - 1));
+  }
+#endif
   norms_and_order<CAP, NT>(sm, Rr, n);
   if (tid == 0) truncation_rule<CAP, NT>(sm, kmin, budget, chi_max);
   bsync<NT>();
@@ -987,3 +1013,13 @@ int launch_fp64_probe(int n_blocks, int64_t iters, double* out, void* stream) {
 }
 
 }  // namespace mpskq
+
+#ifdef MPSKQ_DEBUG_COUNTERS
+extern "C" int mpskq_debug_counters(unsigned long long* out3) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out3, mpskq::g_dbg_rounds, 8);
+  cudaMemcpyFromSymbol(out3 + 1, mpskq::g_dbg_svds, 8);
+  cudaMemcpyFromSymbol(out3 + 2, mpskq::g_dbg_span, 8);
+  return 0;
+}
+#endif
