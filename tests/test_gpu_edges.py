@@ -89,3 +89,20 @@ def test_mixed_capacity_batches_and_reference_states():
     K = P.compute_gram(host, b, "test").entries
     Ko = O.gram([s.sites for s in ref], [s.sites for s in _oracle_states(X, 10, 2, 2, 0.5, 1e-24)], "test")
     assert np.abs(K - Ko).max() < 1e-12
+
+
+def test_benchmark_payload_memory_series_matches_oracle():
+    """benchmark_rows mirrors cmd_benchmark's payload (cli.py:240-294): the
+    per-gate memory series and max chi equal the oracle's (= reference's)."""
+    import paper_2411_09336_b200 as P
+    from paper_2411_09336_b200.benchmark import benchmark_rows
+
+    X = np.random.default_rng(12).uniform(0.0, 2.0, (5, 12))
+    cfg = P.FeatureMapConfig(12, 2, 2, 0.5)
+    out = benchmark_rows(X, cfg)
+    ref = [O.simulate_gates(O.feature_map_gates(x, 12, 2, 2, 0.5), 12, 1e-24, record_memory=True) for x in X]
+    assert out["memory_bytes_per_gate"] == [r.memory for r in ref]
+    assert out["max_chi"] == [max(r.peak, max(r.bond_dims())) for r in ref]
+    assert len(out["inner_product_seconds"]) == 10 and out["simulation_summary"]["median"] > 0
+    with pytest.raises(ValueError):
+        benchmark_rows(X[:1], cfg)
