@@ -96,6 +96,70 @@ __global__ void block_narrow_kernel(const int32_t* __restrict__ chi, const int32
   }
 }
 
+// Greedy refinement of the key order, one CTA per group of kClusterGroup
+// consecutive (key-sorted) kets: each 32-ket block starts from the remaining
+// ket with the most chi = 4 bonds and repeatedly takes the ket that adds the
+// fewest new chi = 4 bonds to the block's union, so more (block, bond) pairs
+// are "narrow" (the kernel's padded work shrinks; results do not change).
+// Ties go to the lowest position, so the order is deterministic.
+constexpr int kClusterGroup = 512;
+constexpr int kClusterMaxWords = 16;  // bonds <= 512 (32 KB of bit rows); longer chains keep the key order
+
+__device__ __forceinline__ unsigned long long block_min_u64(unsigned long long v, unsigned long long* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(kFull, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  v = red[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = min(v, red[w]);
+  return v;
+}
+
+__global__ void __launch_bounds__(kClusterGroup) cluster_kets_kernel(const int32_t* __restrict__ chi, int m,
+                                                                     int64_t n, const int32_t* __restrict__ in,
+                                                                     int32_t* __restrict__ out) {
+  __shared__ uint32_t S[kClusterGroup * kClusterMaxWords];
+  __shared__ uint32_t U[kClusterMaxWords], D[kClusterMaxWords];
+  __shared__ unsigned long long red[kClusterGroup / 32];
+  const int W = (m + 1 + 31) / 32;
+  const int64_t g0 = (int64_t)blockIdx.x * kClusterGroup;
+  const int gs = (int)(n - g0 < kClusterGroup ? n - g0 : kClusterGroup);
+  const int c = threadIdx.x;
+  int cnt = 0;
+  if (c < gs) {
+    const int32_t* row = chi + (int64_t)in[g0 + c] * (m + 1);
+    for (int w = 0; w < W; ++w) {
+      uint32_t word = 0;
+      for (int b = 0; b < 32 && w * 32 + b <= m; ++b) word |= (uint32_t)(row[w * 32 + b] >= kP) << b;
+      S[c * W + w] = word;
+      cnt += __popc(word);
+    }
+  }
+  bool alive = c < gs;
+  int cost = 0;
+  for (int pos = 0; pos < gs; ++pos) {
+    const bool seed = (pos & (kLanes - 1)) == 0;
+    unsigned long long key = ~0ull;
+    if (alive) key = ((unsigned long long)(seed ? 0xFFFF - cnt : cost) << 32) | (unsigned)c;
+    const int j = (int)(block_min_u64(key, red) & 0xFFFFFFFFu);
+    if (c < W) {
+      const uint32_t u = seed ? 0u : U[c];
+      const uint32_t d = S[j * W + c] & ~u;
+      D[c] = d;
+      U[c] = u | d;
+    }
+    if (c == j) {
+      alive = false;
+      out[g0 + pos] = in[g0 + c];
+    }
+    __syncthreads();
+    if (alive) {
+      if (seed) cost = cnt;
+      for (int w = 0; w < W; ++w) cost -= __popc(S[c * W + w] & D[w]);
+    }
+  }
+}
+
 __global__ void invert_perm_kernel(const int32_t* __restrict__ perm, int64_t n, int32_t* __restrict__ inv) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
     inv[perm[p]] = (int32_t)p;
@@ -178,52 +242,48 @@ struct O1Args {
 // instruction cache although the 8 warps run different bra shapes):
 //   phase 1  T[al][p][br] = sum_kb env[al][kb] B[kb][p][br]     al < NA (template)
 //   phase 2  env'[ar][br] = sum_{al,p} conj(A[al][p][ar]) T[al][p][br]
-//            in al blocks guarded by the bra's chi_s; ar runs over 2 or 4 rows
-//            (the bra's chi_{s+1} <= 2 or not)
-// The bra's bond dims are exact (warp-uniform); kb/br run over the zero-padded
-// 4 because the 32 kets of a warp rarely share a smaller bound.
+//            in al blocks guarded by the bra's chi_s; ar runs over 2, 3 or 4
+//            rows (the bra's chi_{s+1})
+// The bra's bond dims are exact (warp-uniform).  kb / br run over the zero
+// padded 4 unless every ket of the 32-ket block has chi <= 3 at that bond
+// (the block "narrow" flags of bonds s and s+1); the br = 3 column is a
+// separate guarded pass so skipping it costs one uniform branch.  Skipped
+// terms are exact zeros, so the result is bitwise independent of the flags.
+template <int NA, int B0, int NB>
+__device__ __forceinline__ void o1_phase1_cols(const double2 (&env)[kP][kP], const double2* B, bool narrow_l,
+                                               double2 (&T)[kP][2][kP]) {
+#pragma unroll
+  for (int kb = 0; kb < kP; ++kb) {
+    if (kb == kP - 1 && narrow_l) break;  // every ket of the block has chi_s <= 3
+    double2 b[2][NB];
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+      for (int c = 0; c < NB; ++c) b[p][c] = B[((kb * 2 + p) * kP + B0 + c) * kLanes];
+#pragma unroll
+    for (int al = 0; al < NA; ++al)
+#pragma unroll
+      for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int c = 0; c < NB; ++c)
+          T[al][p][B0 + c] = cfma(env[al][kb], b[p][c], T[al][p][B0 + c]);
+  }
+}
+
 template <int NA>
-__device__ __forceinline__ void o1_phase1(const double2 (&env)[kP][kP], const double2* B, bool narrow,
-                                          double2 (&T)[kP][2][kP]) {
+__device__ __forceinline__ void o1_phase1(const double2 (&env)[kP][kP], const double2* B, bool narrow_l,
+                                          bool narrow_r, double2 (&T)[kP][2][kP]) {
 #pragma unroll
   for (int al = 0; al < NA; ++al)
 #pragma unroll
     for (int p = 0; p < 2; ++p)
 #pragma unroll
       for (int br = 0; br < kP; ++br) T[al][p][br] = make_double2(0.0, 0.0);
-#pragma unroll
-  for (int kb = 0; kb < kP; ++kb) {
-    if (kb == kP - 1 && narrow) break;  // every ket of the block has chi_s <= 3
-    double2 b[2][kP];
-#pragma unroll
-    for (int p = 0; p < 2; ++p)
-#pragma unroll
-      for (int br = 0; br < kP; ++br) b[p][br] = B[((kb * 2 + p) * kP + br) * kLanes];
-#pragma unroll
-    for (int al = 0; al < NA; ++al)
-#pragma unroll
-      for (int p = 0; p < 2; ++p)
-#pragma unroll
-        for (int br = 0; br < kP; ++br) T[al][p][br] = cfma(env[al][kb], b[p][br], T[al][p][br]);
-  }
+  o1_phase1_cols<NA, 0, kP - 1>(env, B, narrow_l, T);
+  if (!narrow_r) o1_phase1_cols<NA, kP - 1, 1>(env, B, narrow_l, T);
 }
 
-template <int R0, int NR>
-__device__ __forceinline__ void o1_phase2_rows(const double2* Aal, const double2 (&T)[kP][2][kP],
-                                               double2 (&env)[kP][kP]) {
-#pragma unroll
-  for (int p = 0; p < 2; ++p) {
-    double2 av[NR];
-#pragma unroll
-    for (int r = 0; r < NR; ++r) av[r] = Aal[p * kP + R0 + r];
-#pragma unroll
-    for (int r = 0; r < NR; ++r)
-#pragma unroll
-      for (int br = 0; br < kP; ++br) env[R0 + r][br] = cfmac(av[r], T[0][p][br], env[R0 + r][br]);
-  }
-}
-
-template <int AL, int R0, int NR>
+template <int AL, int R0, int NR, int B0, int NB>
 __device__ __forceinline__ void o1_phase2_rows(const double2* A, const double2 (&T)[kP][2][kP],
                                                double2 (&env)[kP][kP]) {
 #pragma unroll
@@ -234,28 +294,36 @@ __device__ __forceinline__ void o1_phase2_rows(const double2* A, const double2 (
 #pragma unroll
     for (int r = 0; r < NR; ++r)
 #pragma unroll
-      for (int br = 0; br < kP; ++br) env[R0 + r][br] = cfmac(av[r], T[AL][p][br], env[R0 + r][br]);
+      for (int c = 0; c < NB; ++c)
+        env[R0 + r][B0 + c] = cfmac(av[r], T[AL][p][B0 + c], env[R0 + r][B0 + c]);
   }
 }
 
-template <int AL>
+template <int AL, int B0, int NB>
 __device__ __forceinline__ void o1_phase2_al(const double2* A, const double2 (&T)[kP][2][kP], int na1,
                                              double2 (&env)[kP][kP]) {
-  o1_phase2_rows<AL, 0, 2>(A, T, env);
-  if (na1 > 2) o1_phase2_rows<AL, 2, 1>(A, T, env);
-  if (na1 > 3) o1_phase2_rows<AL, 3, 1>(A, T, env);
+  o1_phase2_rows<AL, 0, 2, B0, NB>(A, T, env);
+  if (na1 > 2) o1_phase2_rows<AL, 2, 1, B0, NB>(A, T, env);
+  if (na1 > 3) o1_phase2_rows<AL, 3, 1, B0, NB>(A, T, env);
+}
+
+template <int B0, int NB>
+__device__ __forceinline__ void o1_phase2_cols(const double2* A, const double2 (&T)[kP][2][kP], int na,
+                                               int na1, double2 (&env)[kP][kP]) {
+  o1_phase2_al<0, B0, NB>(A, T, na1, env);
+  if (na > 1) o1_phase2_al<1, B0, NB>(A, T, na1, env);
+  if (na > 2) o1_phase2_al<2, B0, NB>(A, T, na1, env);
+  if (na > 3) o1_phase2_al<3, B0, NB>(A, T, na1, env);
 }
 
 __device__ __forceinline__ void o1_phase2(const double2* A, const double2 (&T)[kP][2][kP], int na, int na1,
-                                          double2 (&env)[kP][kP]) {
+                                          bool narrow_r, double2 (&env)[kP][kP]) {
 #pragma unroll
   for (int ar = 0; ar < kP; ++ar)
 #pragma unroll
     for (int br = 0; br < kP; ++br) env[ar][br] = make_double2(0.0, 0.0);
-  o1_phase2_al<0>(A, T, na1, env);
-  if (na > 1) o1_phase2_al<1>(A, T, na1, env);
-  if (na > 2) o1_phase2_al<2>(A, T, na1, env);
-  if (na > 3) o1_phase2_al<3>(A, T, na1, env);
+  o1_phase2_cols<0, kP - 1>(A, T, na, na1, env);
+  if (!narrow_r) o1_phase2_cols<kP - 1, 1>(A, T, na, na1, env);
 }
 
 // One CTA = 8 bras (warps) x 32 kets (lanes); one thread owns one pair's 4x4
@@ -351,15 +419,15 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
       mbar_wait(&full[buf], (it / kStages) & 1);
       const double2* B = sket + buf * kEnt * kLanes + lane;  // B[e] at B[e * 32]
       const double2* A = sbra + buf * kWarpsO1 * kEnt + warp * kEnt;
+      const bool nar_l = __ldg(narrow + s) != 0, nar_r = __ldg(narrow + s + 1) != 0;
       double2 T[kP][2][kP];
-      const bool nar = __ldg(narrow + s) != 0;
       switch (na) {
-        case 1: o1_phase1<1>(env, B, nar, T); break;
-        case 2: o1_phase1<2>(env, B, nar, T); break;
-        case 3: o1_phase1<3>(env, B, nar, T); break;
-        default: o1_phase1<4>(env, B, nar, T); break;
+        case 1: o1_phase1<1>(env, B, nar_l, nar_r, T); break;
+        case 2: o1_phase1<2>(env, B, nar_l, nar_r, T); break;
+        case 3: o1_phase1<3>(env, B, nar_l, nar_r, T); break;
+        default: o1_phase1<4>(env, B, nar_l, nar_r, T); break;
       }
-      o1_phase2(A, T, na, na1, env);
+      o1_phase2(A, T, na, na1, nar_r, env);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[buf]);
       ++it;
@@ -629,6 +697,18 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
   }
   cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, static_cast<uint32_t*>(keys), static_cast<uint32_t*>(keys2),
                                   static_cast<int32_t*>(vals), static_cast<int32_t*>(perm), (int)a.n_kets, 0, 32, st);
+  if ((m + 1 + 31) / 32 <= kClusterMaxWords) {
+    void* refined = nullptr;
+    if ((s_ = alloc(&refined, sizeof(int32_t) * a.n_kets, "refined perm"))) {
+      release();
+      return s_;
+    }
+    const int groups = (int)((a.n_kets + kClusterGroup - 1) / kClusterGroup);
+    if (groups > 0)
+      cluster_kets_kernel<<<groups, kClusterGroup, 0, st>>>(a.ket_chi, m, a.n_kets, static_cast<const int32_t*>(perm),
+                                                             static_cast<int32_t*>(refined));
+    perm = refined;
+  }
   const int32_t* kperm = static_cast<const int32_t*>(perm);
   const int32_t* bperm = train ? kperm : nullptr;
   void *kinv = nullptr, *ordered = nullptr;
