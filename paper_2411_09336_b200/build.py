@@ -18,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libmpskq.so"
 SOURCES = ["runtime.cpp", "encode.cu", "sim.cu", "overlap.cu"]
-HEADERS = ["internal.h", "device.cuh"]
+HEADERS = ["internal.h", "device.cuh", "o1_site.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
