@@ -43,25 +43,30 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile every CUDA/C++ source into one shared library (sm_100a only)."""
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines: tuple = ()) -> Path:
+    """Compile every CUDA/C++ source into one shared library (sm_100a only).
+
+    `out` / `defines` build a variant next to the tree for A/B and debug runs
+    (e.g. ``defines=("MPSKQ_DEBUG_COUNTERS",)``); the product library is LIB."""
+    target = Path(out) if out is not None else LIB
+    if out is None and not defines and not force and not _stale():
         return LIB
     objs = []
-    tmp = PKG / "_obj"
+    tmp = PKG / ("_obj" if not defines else "_obj_" + "_".join(d.lower() for d in defines))
     tmp.mkdir(exist_ok=True)
     for src in SOURCES:
         obj = tmp / (src + ".o")
-        cmd = [_nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [_nvcc(), *NVCC_FLAGS, *(f"-D{d}" for d in defines), "-I", str(ROOT / "include"), "-c",
+               str(CSRC / src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
         objs.append(str(obj))
-    out = LIB.with_suffix(".so.tmp")
-    cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(out), *objs]
+    tmp_out = target.with_suffix(".so.tmp")
+    cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp_out), *objs]
     subprocess.run(cmd, check=True)
-    os.replace(out, LIB)
-    return LIB
+    os.replace(tmp_out, target)
+    return target
 
 
 if __name__ == "__main__":

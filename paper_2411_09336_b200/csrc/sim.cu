@@ -31,10 +31,31 @@ __device__ constexpr double kNoiseFloor = 10.0 * DBL_EPSILON;
 // 1/sqrt(2) exactly as the reference rounds it: _H_MATRIX = [[1,1],[1,-1]]/sqrt(2)
 __device__ constexpr double kInvSqrt2 = 0.7071067811865475;
 constexpr int kMaxSweeps = 40;
+// QR preconditioning of the two-qubit SVD from this many columns up (below it
+// the direct Jacobi needs only ~3 sweeps and the QR would not pay)
+constexpr int kPrecondMinCols = 8;
+template <int CAP>
+struct kPrecondition {
+#ifdef MPSKQ_NO_PRECOND  // A/B builds only
+  static constexpr bool value = false;
+#else
+  static constexpr bool value = CAP >= 8;
+#endif
+};
 
 #ifdef MPSKQ_DEBUG_COUNTERS
 // debug builds only: Jacobi rounds and two-qubit SVDs, summed over states
 __device__ unsigned long long g_dbg_rounds = 0, g_dbg_svds = 0, g_dbg_span = 0;
+// SM cycles per phase (thread 0 of each state): 0 theta build, 1 QRCP + R^H,
+// 2 Jacobi, 3 norms + truncation, 4 C-side write + replay, 5 Q application,
+// 6 W-side write, 7 QR moves
+__device__ unsigned long long g_dbg_cyc[8] = {};
+#define MPSKQ_DBG_T(var) const long long var = clock64()
+#define MPSKQ_DBG_ADD(slot, t0) \
+  if (ltid<NT>() == 0) atomicAdd(&g_dbg_cyc[slot], (unsigned long long)(clock64() - (t0)))
+#else
+#define MPSKQ_DBG_T(var)
+#define MPSKQ_DBG_ADD(slot, t0)
 #endif
 
 // thread index within the state's thread group: NT <= 32 kernels carry one
@@ -82,21 +103,23 @@ struct Smem {
   double2* W;    // LD x LD, column-major: Jacobi rotations / Q / staging
   double2* S;    // 2*CAP*CAP: staging of the neighbour site during QR moves
   double2* rd;   // LD: diagonal of R
+  double2* ud;   // LD: diagonal entries of the pivoted QR's reflectors
   double* tau;   // LD
   double* sig;   // LD
   double* red;   // 32
   double* scal;  // 4: factor, discarded
   int* perm;     // LD
+  int* piv;      // LD: inverse column order of the pivoted QR
   int* ibuf;     // 4: keep
   int* chi;      // m + 1
   double4* rlog;  // per-CTA rotation log (capacities > 32 only)
 
   __host__ __device__ static size_t bytes(int m) {
     size_t b = GlobalWs<CAP>::value
-                   ? sizeof(double2) * LD
-                   : sizeof(double2) * ((LogW<CAP>::value ? 1 : 2) * LD * LD + 2 * CAP * CAP + LD);
+                   ? sizeof(double2) * 2 * LD
+                   : sizeof(double2) * ((LogW<CAP>::value ? 1 : 2) * LD * LD + 2 * CAP * CAP + 2 * LD);
     b += sizeof(double) * (2 * LD + 32 + 4);
-    b += sizeof(int) * (LD + 4 + m + 1);
+    b += sizeof(int) * (2 * LD + 4 + m + 1);
     return (b + 15) & ~size_t(15);
   }
   // gws: this CTA's global workspace (capacities > 48 only)
@@ -119,6 +142,8 @@ struct Smem {
     }
     rd = reinterpret_cast<double2*>(p);
     p += sizeof(double2) * LD;
+    ud = reinterpret_cast<double2*>(p);
+    p += sizeof(double2) * LD;
     tau = reinterpret_cast<double*>(p);
     p += sizeof(double) * LD;
     sig = reinterpret_cast<double*>(p);
@@ -128,6 +153,8 @@ struct Smem {
     scal = reinterpret_cast<double*>(p);
     p += sizeof(double) * 4;
     perm = reinterpret_cast<int*>(p);
+    p += sizeof(int) * LD;
+    piv = reinterpret_cast<int*>(p);
     p += sizeof(int) * LD;
     ibuf = reinterpret_cast<int*>(p);
     p += sizeof(int) * 4;
@@ -218,6 +245,235 @@ template <int CAP, int NT>
 __device__ __forceinline__ double2 r_entry(const Smem<CAP, NT>& sm, int kk, int c) {
   constexpr int LD = 2 * CAP;
   return c == kk ? sm.rd[kk] : sm.A[c * LD + kk];
+}
+
+// ---------------------------------------------------------------------------
+// QR-preconditioned SVD (Drmac-Veselic): for the Jacobi input C (Rr x n) the
+// two-qubit step factors B = C^H with column pivoting, B P = Q R, and runs the
+// one-sided Jacobi on X = R^H (Rr x k), which is close to column-orthogonal
+// already: 6-7 sweeps instead of 13-20 on the 60..90-column thetas of d = 8
+// (numpy replica of this Jacobi on reference thetas).  With X W' = Z:
+//   C = P R^H Q^H = (P Z) (Q W')^H,
+// so the scaled side is P Z (rows permuted) and the orthonormal side Q W'
+// (reflectors applied to W'), the same roles C W and W play unpreconditioned.
+
+// group-wide argmax of (v, idx), ties to the smaller idx; `red` needs 32 doubles
+template <int NT>
+__device__ __forceinline__ int block_argmax(double v, int idx, double* red) {
+  const unsigned mask = group_mask<NT>();
+  constexpr int G = NT < 32 ? NT : 32;
+#pragma unroll
+  for (int o = G >> 1; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(mask, v, o);
+    const int oi = __shfl_xor_sync(mask, idx, o);
+    if (ov > v || (ov == v && oi < idx)) {
+      v = ov;
+      idx = oi;
+    }
+  }
+  if constexpr (NT > 32) {
+    static_assert(NT <= 512, "red holds 16 warps");
+    const int w = threadIdx.x >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+      red[w] = v;
+      red[16 + w] = (double)idx;
+    }
+    __syncthreads();
+    v = red[0];
+    idx = (int)red[16];
+#pragma unroll
+    for (int i = 1; i < NT / 32; ++i) {
+      const double ov = red[i];
+      const int oi = (int)red[16 + i];
+      if (ov > v || (ov == v && oi < idx)) {
+        v = ov;
+        idx = oi;
+      }
+    }
+  }
+  return idx;
+}
+
+// packed offset of reflector j's strictly-lower part (rows j+1..nr-1)
+__device__ __forceinline__ int refl_off(int j, int nr) { return j * (nr - 1) - ((j * (j - 1)) >> 1); }
+
+// Householder QR with column pivoting of B (nr x nc, column-major in A):
+// B P = Q R.  Pivot = largest trailing column norm (recomputed exactly in the
+// update pass), ties to the lower index.  On return: R's strict upper part in
+// A, its diagonal in rd; reflector j is ud[j] (row j) and S[refl_off(j)...]
+// (rows j+1..nr-1) with tau[j]; piv[c] = position of original column c.
+template <int CAP, int NT>
+__device__ __noinline__ int householder_qrcp(Smem<CAP, NT>& sm, int nr, int nc) {
+  constexpr int LD = 2 * CAP;
+  const int tid = ltid<NT>();
+  const int k = min(nr, nc);
+  const unsigned msk = group_mask<NT>();
+  double2* A = sm.A;
+  {
+    const int G = group_width<NT>(nc), per = NT / G;
+    for (int base = 0; base < nc; base += per) {
+      const int c = base + tid / G, g = tid % G;
+      double acc = 0.0;
+      if (c < nc)
+        #pragma unroll 1
+        for (int r = g; r < nr; r += G) acc += cnorm2(A[c * LD + r]);
+      acc = group_sum(acc, G, msk);
+      if (c < nc && g == 0) {
+        sm.sig[c] = acc;
+        sm.perm[c] = c;  // original column at each position
+      }
+    }
+  }
+  bsync<NT>();
+  for (int j = 0; j < k; ++j) {
+    double bv = -1.0;
+    int bi = 1 << 30;
+    #pragma unroll 1
+    for (int c = j + tid; c < nc; c += NT) {
+      const double v = sm.sig[c];
+      if (v > bv) {
+        bv = v;
+        bi = c;
+      }
+    }
+    const int pv = block_argmax<NT>(bv, bi, sm.red);
+    // every thread reads the pivot's trailing norm and leading entry before the
+    // swap and derives the reflector itself: one barrier per step fewer
+    const double nx2 = sm.sig[pv];
+    const double2 x1 = A[pv * LD + j];
+    if (pv != j) {
+      bsync<NT>();  // everyone has read sig[pv] / x1
+      #pragma unroll 1
+      for (int r = tid; r < nr; r += NT) {
+        const double2 t = A[j * LD + r];
+        A[j * LD + r] = A[pv * LD + r];
+        A[pv * LD + r] = t;
+      }
+      if (tid == 0) {
+        sm.sig[pv] = sm.sig[j];
+        const int tp = sm.perm[j];
+        sm.perm[j] = sm.perm[pv];
+        sm.perm[pv] = tp;
+      }
+    }
+    const double nx = sqrt(nx2);
+    const double ax1 = hypot(x1.x, x1.y);
+    double tau = 0.0;
+    double2 uj = x1;
+    if (nx > 0.0) {
+      const double2 ph = ax1 > 0.0 ? make_double2(x1.x / ax1, x1.y / ax1) : make_double2(1.0, 0.0);
+      uj = make_double2(x1.x + ph.x * nx, x1.y + ph.y * nx);
+      tau = 1.0 / (nx * (nx + ax1));
+      if (tid == 0) sm.rd[j] = make_double2(-ph.x * nx, -ph.y * nx);
+    } else if (tid == 0) {
+      sm.rd[j] = cz();
+    }
+    if (tid == 0) {
+      sm.tau[j] = tau;
+      sm.sig[j] = nx2;
+    }
+    bsync<NT>();  // the swap is complete
+    if (tid == 0) A[j * LD + j] = uj;  // read below only through uj
+    // apply H_j to columns j+1..nc-1 and refresh their trailing norms (rows > j)
+    const int c0 = j + 1, ncols = nc - c0;
+    if (ncols > 0) {
+      const double2* u = A + j * LD;
+      const int G = group_width<NT>(ncols), per = NT / G;
+      for (int base = 0; base < ncols; base += per) {
+        const int ci = base + tid / G, g = tid % G;
+        const bool act = ci < ncols;
+        const int c = c0 + (act ? ci : 0);
+        double2 acc = cz();
+        if (act && tau != 0.0)
+          #pragma unroll 1
+          for (int r = j + g; r < nr; r += G) acc = cfmac(r == j ? uj : u[r], A[c * LD + r], acc);
+        acc = group_sum(acc, G, msk);
+        double nrm = 0.0;
+        if (act) {
+          const double2 w = cscale(acc, tau);
+          #pragma unroll 1
+          for (int r = j + g; r < nr; r += G) {
+            double2 v = A[c * LD + r];
+            if (tau != 0.0) {
+              v = csub(v, cmul(r == j ? uj : u[r], w));
+              A[c * LD + r] = v;
+            }
+            if (r > j) nrm += cnorm2(v);
+          }
+        }
+        nrm = group_sum(nrm, G, msk);
+        if (act && g == 0) sm.sig[c] = nrm;
+      }
+    }
+    bsync<NT>();
+  }
+  // stash the reflectors (A's lower part is about to hold R^H), invert the order
+  #pragma unroll 1
+  for (int idx = tid; idx < k * nr; idx += NT) {
+    const int j = idx / nr, r = idx - j * nr;
+    if (r == j)
+      sm.ud[j] = A[j * LD + j];
+    else if (r > j)
+      sm.S[refl_off(j, nr) + r - j - 1] = A[j * LD + r];
+  }
+  #pragma unroll 1
+  for (int c = tid; c < nc; c += NT) sm.piv[sm.perm[c]] = c;
+  bsync<NT>();
+  return k;
+}
+
+// A := R^H (nc x k, lower trapezoidal) from the QRCP's R (k x nc) in place
+template <int CAP, int NT>
+__device__ void form_rh(Smem<CAP, NT>& sm, int nc, int k) {
+  constexpr int LD = 2 * CAP;
+  const int tid = ltid<NT>();
+  double2* A = sm.A;
+  #pragma unroll 1
+  for (int idx = tid; idx < k * nc; idx += NT) {
+    const int j = idx / nc, c = idx - j * nc;
+    if (c > j) A[j * LD + c] = cconj(A[c * LD + j]);  // R(j, c) lives in row j, column c
+  }
+  bsync<NT>();
+  #pragma unroll 1
+  for (int idx = tid; idx < k * k; idx += NT) {
+    const int j = idx / k, c = idx - j * k;
+    if (c < j)
+      A[j * LD + c] = cz();
+    else if (c == j)
+      A[j * LD + j] = cconj(sm.rd[j]);
+  }
+  bsync<NT>();
+}
+
+// M (nr x kc, column-major, ld LD) := H_0 ... H_{k-1} M with the stashed reflectors
+template <int CAP, int NT>
+__device__ __noinline__ void apply_q_packed(Smem<CAP, NT>& sm, double2* M, int nr, int k, int kc) {
+  constexpr int LD = 2 * CAP;
+  const int tid = ltid<NT>();
+  const unsigned msk = group_mask<NT>();
+  const int G = group_width<NT>(kc), per = NT / G;
+  for (int j = k - 1; j >= 0; --j) {
+    const double tau = sm.tau[j];
+    if (tau == 0.0) continue;  // uniform
+    const double2 u0 = sm.ud[j];
+    const double2* us = sm.S + refl_off(j, nr) - j - 1;  // us[r] for r > j
+    for (int base = 0; base < kc; base += per) {
+      const int c = base + tid / G, g = tid % G;
+      const bool act = c < kc;
+      double2 acc = cz();
+      if (act)
+        #pragma unroll 1
+        for (int r = j + g; r < nr; r += G) acc = cfmac(r == j ? u0 : us[r], M[c * LD + r], acc);
+      acc = group_sum(acc, G, msk);
+      if (act) {
+        const double2 w = cscale(acc, tau);
+        #pragma unroll 1
+        for (int r = j + g; r < nr; r += G) M[c * LD + r] = csub(M[c * LD + r], cmul(r == j ? u0 : us[r], w));
+      }
+    }
+    bsync<NT>();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -606,6 +862,7 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
   double2* Y = st.base + st.off[q + 1];
   const int Mr = 2 * chl, Nc = 2 * chr;
   constexpr bool kLog = LogW<CAP>::value;
+  MPSKQ_DBG_T(t_build);
   const double2* Xs = X;  // capacities > 32 read the sites straight from L1/L2
   const double2* Ys = Y;
   if constexpr (!kLog) {
@@ -623,6 +880,11 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
   // (:184-186); every item produces the two entries the gate couples.
   const double c = cs.x, s = cs.y;
   const bool rxx = code == MPSKQ_OP_RXX;
+  const int Rr = left ? Mr : Nc;
+  const int n = left ? Nc : Mr;
+  const int kmin = min(Mr, Nc);
+  const bool pre = kPrecondition<CAP>::value && kmin >= kPrecondMinCols;
+  const bool theta_cm = left != pre;  // store C (not preconditioned) or C^H
   int bad = 0;
   #pragma unroll 1
   for (int it = tid; it < chl * chr * 2; it += NT) {
@@ -649,10 +911,10 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
       o2 = T1;
     }
     bad |= !(cfinite(o1) && cfinite(o2));
-    if (left) {  // C = theta
+    if (theta_cm) {  // theta, column-major
       sm.A[col1 * LD + row1] = o1;
       sm.A[col2 * LD + row2] = o2;
-    } else {  // C = theta^H
+    } else {  // theta^H, column-major
       sm.A[row1 * LD + col1] = cconj(o1);
       sm.A[row2 * LD + col2] = cconj(o2);
     }
@@ -661,49 +923,77 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
     st.status = MPSKQ_STATE_NONFINITE;
     return;
   }
-  // left: theta V = U S  (W = V);  right: theta^H U = V S  (W = U)
-  const int Rr = left ? Mr : Nc;
-  const int n = left ? Nc : Mr;
-  const int kmin = min(Mr, Nc);
-  const int sweeps = jacobi<CAP, NT>(sm, Rr, n);
+  // Jacobi input C: left: theta V = U S  (W = V);  right: theta^H U = V S  (W = U).
+  // Preconditioned: A holds B = C^H; QRCP, then the Jacobi runs on R^H.
+  MPSKQ_DBG_ADD(0, t_build);
+  MPSKQ_DBG_T(t_qr);
+  int ncol = n;
+  if (pre) {
+    householder_qrcp<CAP, NT>(sm, n, Rr);
+    form_rh<CAP, NT>(sm, Rr, kmin);
+    ncol = kmin;
+  }
+  MPSKQ_DBG_ADD(1, t_qr);
+  MPSKQ_DBG_T(t_jac);
+  const int sweeps = jacobi<CAP, NT>(sm, Rr, ncol);
+  MPSKQ_DBG_ADD(2, t_jac);
+  MPSKQ_DBG_T(t_trunc);
 #ifdef MPSKQ_DEBUG_COUNTERS
   if (tid == 0) {
     atomicAdd(&g_dbg_rounds, (unsigned long long)sweeps);
     atomicAdd(&g_dbg_svds, 1ull);
-    atomicAdd(&g_dbg_span, (unsigned long long)(n + (n & 1) - 1));
+    atomicAdd(&g_dbg_span, (unsigned long long)(ncol + (ncol & 1) - 1));
   }
 #endif
-  norms_and_order<CAP, NT>(sm, Rr, n);
+  norms_and_order<CAP, NT>(sm, Rr, ncol);
   if (tid == 0) truncation_rule<CAP, NT>(sm, kmin, budget, chi_max);
   bsync<NT>();
   const int keep = sm.ibuf[0];
   const double factor = sm.scal[0];
+  MPSKQ_DBG_ADD(3, t_trunc);
+  MPSKQ_DBG_T(t_cside);
   if (keep > CAP) {
     st.status = MPSKQ_STATE_CAPACITY;
     return;
   }
-  // C side first (it lives in A), then W (log mode rebuilds it in A)
+  // C side first (it lives in A), then W (log mode rebuilds it in A).
+  // Preconditioned, row r of C is row piv[r] of the rotated R^H.
   if (left) {
     // site_q = U s (mps.py:194)
     #pragma unroll 1
     for (int idx = tid; idx < Mr * keep; idx += NT) {
       const int row = idx / keep, kk = idx - row * keep;
-      X[idx] = cscale(sm.A[sm.perm[kk] * LD + row], factor);
+      X[idx] = cscale(sm.A[sm.perm[kk] * LD + (pre ? sm.piv[row] : row)], factor);
     }
   } else {
     // site_{q+1} = s Vh (mps.py:197-199)
     #pragma unroll 1
     for (int idx = tid; idx < keep * Nc; idx += NT) {
       const int kk = idx / Nc, col = idx - kk * Nc;
-      Y[idx] = cscale(cconj(sm.A[sm.perm[kk] * LD + col]), factor);
+      Y[idx] = cscale(cconj(sm.A[sm.perm[kk] * LD + (pre ? sm.piv[col] : col)]), factor);
     }
   }
-  const double2* Wm = sm.W;
+  double2* Wm = sm.W;
   if constexpr (kLog) {
     bsync<NT>();
-    replay<CAP, NT>(sm, sm.A, n, sweeps);
+    replay<CAP, NT>(sm, sm.A, ncol, sweeps);
     Wm = sm.A;
   }
+  MPSKQ_DBG_ADD(4, t_cside);
+  MPSKQ_DBG_T(t_q);
+  if (pre) {
+    // W = Q [W'; 0] (n x kmin)
+    const int extra = n - kmin;
+    #pragma unroll 1
+    for (int idx = tid; idx < extra * kmin; idx += NT) {
+      const int cc = idx / extra, r = kmin + idx - cc * extra;
+      Wm[cc * LD + r] = cz();
+    }
+    bsync<NT>();
+    apply_q_packed<CAP, NT>(sm, Wm, n, kmin, kmin);
+  }
+  MPSKQ_DBG_ADD(5, t_q);
+  MPSKQ_DBG_T(t_wside);
   if (left) {
     // site_{q+1} = Vh
     #pragma unroll 1
@@ -725,6 +1015,7 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
     st.peak = max(st.peak, keep);
   }
   bsync<NT>();
+  MPSKQ_DBG_ADD(6, t_wside);
 }
 
 
@@ -783,12 +1074,18 @@ __global__ void __launch_bounds__(NT * SpcFor<NT>::value) sim_kernel(SimArgs a) 
           case MPSKQ_OP_RZ:
             op_one_qubit<CAP, NT>(sm, st, op.y, code, cs);
             break;
-          case MPSKQ_OP_QRL:
+          case MPSKQ_OP_QRL: {
+            MPSKQ_DBG_T(t_mv);
             op_qr_left<CAP, NT>(sm, st, op.y);
+            MPSKQ_DBG_ADD(7, t_mv);
             break;
-          case MPSKQ_OP_QRR:
+          }
+          case MPSKQ_OP_QRR: {
+            MPSKQ_DBG_T(t_mv);
             op_qr_right<CAP, NT>(sm, st, op.y);
+            MPSKQ_DBG_ADD(7, t_mv);
             break;
+          }
           default:
             op_two_qubit<CAP, NT>(sm, st, op.y, code, left, cs, a.budget, a.chi_max);
             break;
@@ -1020,6 +1317,12 @@ extern "C" int mpskq_debug_counters(unsigned long long* out3) {
   cudaMemcpyFromSymbol(out3, mpskq::g_dbg_rounds, 8);
   cudaMemcpyFromSymbol(out3 + 1, mpskq::g_dbg_svds, 8);
   cudaMemcpyFromSymbol(out3 + 2, mpskq::g_dbg_span, 8);
+  return 0;
+}
+// 8 per-phase cycle sums (see g_dbg_cyc)
+extern "C" int mpskq_debug_cycles(unsigned long long* out8) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out8, mpskq::g_dbg_cyc, 64);
   return 0;
 }
 #endif
