@@ -14,8 +14,8 @@ int fail(int status, const char* fmt, ...);
 int cuda_fail(int err, const char* what);  // err is a cudaError_t
 
 // chi capacities with a compiled simulation + overlap path
-constexpr int kChiCaps[] = {4, 8, 12, 16, 24, 32, 48, 64, 80, 96};
-constexpr int kNumChiCaps = 10;
+constexpr int kChiCaps[] = {4, 8, 12, 16, 24, 32, 48, 64, 80, 96, 128};
+constexpr int kNumChiCaps = sizeof(kChiCaps) / sizeof(kChiCaps[0]);
 inline bool chi_cap_supported(int c) {
   for (int x : kChiCaps)
     if (x == c) return true;

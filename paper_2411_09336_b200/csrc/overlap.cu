@@ -751,6 +751,7 @@ int launch_overlap(const OverlapArgs& a, void* stream) {
     case 64: s = launch_mma<64>(a, st); break;
     case 80: s = launch_mma<80>(a, st); break;
     case 96: s = launch_mma<96>(a, st); break;
+    case 128: s = launch_mma<128>(a, st); break;
     default: return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", a.chi_cap);
   }
   if (s != MPSKQ_OK) return s;
@@ -774,7 +775,8 @@ void tile_shape(int chi_cap, int* rb, int* cb) {
     case 48: *rb = 1; *cb = MmaCfg<48>::warps; return;
     case 64: *rb = 1; *cb = MmaCfg<64>::warps; return;
     case 80: *rb = 1; *cb = MmaCfg<80>::warps; return;
-    default: *rb = 1; *cb = MmaCfg<96>::warps; return;
+    case 96: *rb = 1; *cb = MmaCfg<96>::warps; return;
+    default: *rb = 1; *cb = MmaCfg<128>::warps; return;
   }
 }
 

@@ -1265,6 +1265,7 @@ int launch_simulate(const SimArgs& a, void* stream) {
     case 64: return launch_sim_cap<64>(a, st);
     case 80: return launch_sim_cap<80>(a, st);
     case 96: return launch_sim_cap<96>(a, st);
+    case 128: return launch_sim_cap<128>(a, st);
   }
   return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", a.chi_cap);
 }
@@ -1282,7 +1283,8 @@ int launch_svd(const SvdArgs& a, void* stream) {
   if (big <= 96) return launch_svd_cap<48>(a, st);
   if (big <= 128) return launch_svd_cap<64>(a, st);
   if (big <= 160) return launch_svd_cap<80>(a, st);
-  return launch_svd_cap<96>(a, st);
+  if (big <= 192) return launch_svd_cap<96>(a, st);
+  return launch_svd_cap<128>(a, st);
 }
 
 // FP64 FMA throughput probe: 16 independent DFMA chains per thread

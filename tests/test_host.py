@@ -27,7 +27,7 @@ def test_abi_version_and_caps(native):
     from paper_2411_09336_b200 import _native
 
     assert native.mpskq_abi_version() == 1
-    assert _native.supported_chi_caps() == [4, 8, 12, 16, 24, 32, 48, 64, 80, 96]
+    assert _native.supported_chi_caps() == [4, 8, 12, 16, 24, 32, 48, 64, 80, 96, 128]
     assert native.mpskq_device_count() >= 0
 
 

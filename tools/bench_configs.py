@@ -25,6 +25,11 @@ CONFIGS = {
     "config5_m100_d4": (100, 4, 0.1, 1e-16, 800),
     "config5_m100_d5": (100, 5, 0.1, 1e-16, 800),
     "config5_m100_d6": (100, 6, 0.1, 1e-16, 800),
+    "config5_m100_d7": (100, 7, 0.1, 1e-16, 800),
+    "config5_m100_d8": (100, 8, 0.1, 1e-16, 800),
+    # headline stretch (paper's largest d at 165 qubits), one wave of states
+    "config4_m165_d6_1e-16": (165, 6, 0.1, 1e-16, 296),
+    "config4_m165_d6_1e-24": (165, 6, 0.1, 1e-24, 148),
 }
 
 
