@@ -412,3 +412,21 @@ def test_integration_md_ctypes_stub_runs():
                                budget=budget).entries
     assert np.abs(Kt - g["K_test"]).max() < 1e-10
     assert rep.n_inner_products == 64 * 63 // 2
+
+
+@pytest.mark.parametrize("cap", [96, 128])
+def test_largest_capacities_match_reference(cap):
+    """The two largest capacities (96, and 128 for the paper's d=6 at 165 qubits
+    with budget 1e-24) on the d=8 rows: same bond dims and peaks as the
+    reference whatever capacity runs them."""
+    import paper_2411_09336_b200 as P
+    from paper_2411_09336_b200.kernel import simulate_rows
+
+    g = golden("config5_m100_d8.npz")
+    cfg, budget = _cfg(g)
+    b = simulate_rows(g["X"], cfg, budget, chi_cap=cap)
+    assert b.chi_cap == cap
+    assert np.array_equal(b.bond_dims(), g["train_chi"])
+    assert np.array_equal(b.peak.cpu().numpy(), g["train_peak"])
+    K = P.compute_gram(b, b, "train").entries
+    assert np.abs(K - g["K_train"]).max() < 1e-6
