@@ -371,11 +371,12 @@ struct MmaCfg {
   static constexpr int L1 = (CAP + 15) / 16 * 16 + 4;       // env plane leading dim
   static constexpr int L2 = (2 * CAP + 15) / 16 * 16 + 4;   // T plane leading dim
   static constexpr int per_warp = 2 * R8 * L1 + 2 * R8 * L2;  // doubles
-  // above ~200 KB per warp (capacities > 48) the planes move to a per-warp
-  // global scratch (L2 resident)
-  static constexpr bool global = (size_t)per_warp * 8 > 200 * 1024;
+  // When fewer than 8 warps' planes fit in shared memory (capacities >= 24)
+  // the planes move to a per-warp global scratch (L2 resident): at capacity
+  // 48/64 the shared-memory variant ran ONE warp per SM (5x slower)
   static constexpr int max_warps = (220 * 1024) / (per_warp * 8);
-  static constexpr int warps = global ? 4 : (max_warps > 16 ? 16 : (max_warps < 1 ? 1 : max_warps));
+  static constexpr bool global = max_warps < 8;
+  static constexpr int warps = global ? 8 : (max_warps > 16 ? 16 : max_warps);
   static constexpr size_t smem = global ? 0 : sizeof(double) * (size_t)per_warp * warps;
 };
 
