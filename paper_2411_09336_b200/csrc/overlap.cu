@@ -30,6 +30,10 @@
 #include "internal.h"
 #include "o1_site.cuh"
 
+#ifndef MPSKQ_MMA_GLOBAL_CTAS
+#define MPSKQ_MMA_GLOBAL_CTAS 2  // resident CTAs per SM of the L2-plane DMMA overlap
+#endif
+
 namespace mpskq {
 
 namespace {
@@ -377,6 +381,7 @@ struct MmaCfg {
   static constexpr int max_warps = (220 * 1024) / (per_warp * 8);
   static constexpr bool global = max_warps < 8;
   static constexpr int warps = global ? 8 : (max_warps > 16 ? 16 : max_warps);
+  static constexpr int ctas_per_sm = global ? MPSKQ_MMA_GLOBAL_CTAS : 1;
   static constexpr size_t smem = global ? 0 : sizeof(double) * (size_t)per_warp * warps;
 };
 
@@ -414,7 +419,7 @@ struct MmaArgs {
 };
 
 template <int CAP>
-__global__ void __launch_bounds__(MmaCfg<CAP>::warps * 32, 1) overlap_mma_kernel(MmaArgs a) {
+__global__ void __launch_bounds__(MmaCfg<CAP>::warps * 32, MmaCfg<CAP>::ctas_per_sm) overlap_mma_kernel(MmaArgs a) {
   using C = MmaCfg<CAP>;
   extern __shared__ __align__(16) double smem_d[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -720,7 +725,7 @@ int launch_mma(const OverlapArgs& a, cudaStream_t st) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = (int)std::min<int64_t>((int64_t)tiles.size(), (int64_t)sms * (C::global ? 2 : 16));
+    const int grid = (int)std::min<int64_t>((int64_t)tiles.size(), (int64_t)sms * (C::global ? 2 * C::ctas_per_sm : 16));
     if (C::global) {
       e = cudaMallocAsync(reinterpret_cast<void**>(&o.gws),
                           sizeof(double) * (size_t)C::per_warp * C::warps * grid, st);
