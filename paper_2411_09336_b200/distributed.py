@@ -24,6 +24,15 @@ import torch
 from . import _native as N
 
 
+# Run the exchange steps even for a single rank (tests drive the NCCL
+# collectives on a one-GPU box this way; multi-GPU runs take them anyway).
+FORCE_COLLECTIVES = False
+
+
+def _exchange(world: int) -> bool:
+    return world > 1 or FORCE_COLLECTIVES
+
+
 def rank_world(group=None) -> tuple:
     import torch.distributed as dist
 
@@ -109,13 +118,13 @@ def gram(X_bras, X_kets, cfg, kind: str, budget: float, chi_max: int = 0, group=
     lo, hi = shard(n_all, world, rank)
     with Timer() as t_sim:
         local = simulate_rows(X_all[lo:hi], cfg, budget, chi_max) if hi > lo else None
-        if world > 1:
+        if _exchange(world):
             cap = torch.tensor([local.chi_cap if local is not None else 0], device="cuda")
             cap = int(_all_reduce_max(cap, group).item())
             if local is not None and local.chi_cap != cap:
                 local = simulate_rows(X_all[lo:hi], cfg, budget, chi_max, chi_cap=cap)
     rep.n_simulations = n_all
-    if world > 1:
+    if _exchange(world):
         from .mps import batch_layout
 
         off, stride = batch_layout(cfg.m, cap)
@@ -146,7 +155,7 @@ def gram(X_bras, X_kets, cfg, kind: str, budget: float, chi_max: int = 0, group=
         K_dev = torch.zeros((nb, nk), dtype=torch.float64, device="cuda")
         overlap_matrix(bras, kets, kind, rank=rank, world=world, out=K_dev)
     t0 = time.perf_counter()
-    if world > 1:
+    if _exchange(world):
         K_dev = _reduce_sum_to0(K_dev, group)
     K = K_dev.cpu().numpy() if rank == 0 else np.empty((0, 0))
     rep._add("simulation", t_sim.seconds())

@@ -63,3 +63,47 @@ def test_two_ranks_on_one_gpu_match_single_process(kind):
     K0 = out[0][0]
     assert np.array_equal(K0, ref)
     assert np.abs(K0 - (g["K_train"] if kind == "train" else g["K_test"])).max() < 1e-10
+
+
+def _nccl_single(kind, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        import paper_2411_09336_b200 as P
+        from paper_2411_09336_b200 import distributed as D
+
+        D.FORCE_COLLECTIVES = True  # all-gather / all-reduce / reduce through NCCL on device tensors
+        g = golden("headline_m165_d1.npz")
+        cfg = P.FeatureMapConfig(165, 2, 1, 0.1)
+        Xb = g["X"] if kind == "train" else g["X_test"]
+        sched = P.make_schedule(len(Xb), len(g["X"]), 1, "round_robin", kind)
+        K = P.run_distributed(Xb, g["X"], cfg, sched, budget=1e-24).entries
+        q.put((dist.get_backend(), K))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["train", "test"])
+def test_nccl_exchange_path_single_gpu(kind):
+    """The NCCL branch of the exchange (device all-gather of the packed slabs
+    and bond dims, all-reduce of the capacity, SUM-reduce of K) on one rank:
+    the only NCCL configuration a one-GPU box can run."""
+    import paper_2411_09336_b200 as P
+
+    g = golden("headline_m165_d1.npz")
+    cfg = P.FeatureMapConfig(165, 2, 1, 0.1)
+    Xb = g["X"] if kind == "train" else g["X_test"]
+    ref = P.run_distributed(Xb, g["X"], cfg, P.make_schedule(len(Xb), len(g["X"]), 1, "round_robin", kind)).entries
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_single, args=(kind, q))
+    p.start()
+    backend, K = q.get(timeout=300)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    assert backend == "nccl"
+    assert np.array_equal(K, ref)
