@@ -28,6 +28,15 @@ from . import _native as N
 # collectives on a one-GPU box this way; multi-GPU runs take them anyway).
 FORCE_COLLECTIVES = False
 
+# How the ranks share MPS: "allgather" (every rank holds all slabs: one
+# exchange, fastest while the slabs fit), "ring" (each rank holds its own
+# shard plus one visiting shard; world-1 point-to-point ring steps, the
+# reference's round-robin schedule kernel.py:188-266, for sets that exceed
+# HBM), or "auto" (ring when the gathered slabs would take more than
+# RING_FRACTION of the smallest free device memory).
+EXCHANGE = "auto"
+RING_FRACTION = 0.4
+
 
 def _exchange(world: int) -> bool:
     return world > 1 or FORCE_COLLECTIVES
@@ -86,6 +95,134 @@ def _reduce_sum_to0(t: torch.Tensor, group=None) -> torch.Tensor:
     return h.to(t.device)
 
 
+def _exchange_mode(n_all: int, local, cap: int, cfg, world: int, group=None) -> str:
+    """The EXCHANGE setting resolved identically on every rank."""
+    if world == 1 or EXCHANGE in ("allgather", "ring"):
+        return EXCHANGE if EXCHANGE != "auto" else "allgather"
+    from .mps import batch_layout
+
+    _, stride = batch_layout(cfg.m, cap)
+    gathered = n_all * 2 * stride * 8
+    free = torch.tensor([float(torch.cuda.mem_get_info()[0])], dtype=torch.float64, device="cuda")
+    import torch.distributed as dist
+
+    h = free.cpu() if _host_collectives(group) else free
+    dist.all_reduce(h, op=dist.ReduceOp.MIN, group=group)
+    return "ring" if gathered > RING_FRACTION * float(h.item()) else "allgather"
+
+
+def _gram_ring(X_bras, X_kets, cfg, kind, budget, chi_max, group, rank, world, local, cap, t_sim, rep):
+    """Ring exchange: bras and kets sharded separately; the ket shards travel."""
+    from ._device import Timer
+    from .kernel import simulate_rows
+
+    train = kind == "train"
+    nb, nk = X_bras.shape[0], X_kets.shape[0]
+    blo, bhi = shard(nb, world, rank)
+    klo, khi = shard(nk, world, rank)
+    with Timer() as t_sim2:
+        if train:
+            kets = local  # the all-gather sharding of the train rows is the same
+            if kets is None or kets.chi_cap != cap:
+                kets = simulate_rows(X_kets[klo:khi], cfg, budget, chi_max, chi_cap=cap)
+            bras = kets
+        else:
+            rows = np.vstack([X_bras[blo:bhi], X_kets[klo:khi]])
+            both = simulate_rows(rows, cfg, budget, chi_max, chi_cap=cap)
+            bras, kets = both.rows(0, bhi - blo), both.rows(bhi - blo, len(both))
+    counts = [shard(nk, world, r)[1] - shard(nk, world, r)[0] for r in range(world)]
+    with Timer() as t_ov:
+        K_dev = torch.zeros((nb, nk), dtype=torch.float64, device="cuda")
+        comm = _ring_gram(kets, bras, blo, counts, cfg, kind, rank, world, group, K_dev)
+    t0 = time.perf_counter()
+    K_dev = _reduce_sum_to0(K_dev, group)
+    K = K_dev.cpu().numpy() if rank == 0 else np.empty((0, 0))
+    rep._add("simulation", t_sim.seconds() + t_sim2.seconds())
+    rep._add("communication", comm)
+    rep._add("inner_products", t_ov.seconds() - comm)
+    rep._add("merge", time.perf_counter() - t0)
+    rep.n_inner_products = nk * (nk - 1) // 2 if train else nb * nk
+    return K, rep
+
+
+def ring_plan(world: int, rank: int, kind: str) -> list:
+    """(step, held shard, block) for every ring step of `rank`.  At step t the
+    rank holds ket shard (rank - t) mod world.  block is "diag" (train, own
+    shard: triangle + unit diagonal), "full" (bras of this rank x held kets;
+    train mirrors it) or None.  For train each unordered shard pair is
+    computed exactly once: ring distance t < world/2 by the holder, and at
+    t == world/2 (even world) only by ranks < world/2."""
+    plan = []
+    for t in range(world):
+        held = (rank - t) % world
+        if kind != "train":
+            plan.append((t, held, "full"))
+        elif t == 0:
+            plan.append((t, held, "diag"))
+        elif 2 * t < world or (2 * t == world and rank < world // 2):
+            plan.append((t, held, "full"))
+        else:
+            plan.append((t, held, None))
+    return plan
+
+
+def _ring_shift(tensors: list, rank: int, world: int, group=None) -> list:
+    """Send every tensor to rank+1 and receive same-shaped ones from rank-1."""
+    import torch.distributed as dist
+
+    host = _host_collectives(group)
+    src = [t.cpu() if host else t for t in tensors]
+    dst = [torch.empty_like(t) for t in src]
+    ops = []
+    for a, b in zip(src, dst):
+        ops.append(dist.P2POp(dist.isend, a, (rank + 1) % world, group))
+        ops.append(dist.P2POp(dist.irecv, b, (rank - 1) % world, group))
+    for w in dist.batch_isend_irecv(ops):
+        w.wait()
+    dev = tensors[0].device
+    return [b.to(dev) for b in dst]
+
+
+def _ring_gram(full_kets, bras, nb_lo, kets_counts, cfg, kind, rank, world, group, K_dev):
+    """Fill this rank's ring blocks of K_dev; returns seconds spent exchanging."""
+    from .mps import MpsBatch, overlap_matrix
+
+    mx = max(kets_counts)
+    pad_sites = full_kets.sites.new_zeros((mx, full_kets.sites.shape[1]))
+    pad_chi = full_kets.chi.new_zeros((mx, full_kets.chi.shape[1]))
+    pad_sites[: len(full_kets)] = full_kets.sites
+    pad_chi[: len(full_kets)] = full_kets.chi
+    offs = np.concatenate([[0], np.cumsum(kets_counts)])
+    comm = 0.0
+    # every rank shifts the same number of times: train needs ring distances
+    # up to world // 2, test all of them
+    plan = ring_plan(world, rank, kind)[: (world // 2 + 1 if kind == "train" else world)]
+    for t, held, block in plan:
+        c = kets_counts[held]
+        if block is not None and c > 0 and len(bras) > 0:
+            kets = MpsBatch(cfg.m, full_kets.chi_cap, full_kets.site_off, full_kets.stride, pad_sites[:c],
+                            pad_chi[:c], pad_sites.new_zeros(c), pad_chi.new_zeros(c), full_kets.budget,
+                            full_kets.gate_count_1q, full_kets.gate_count_2q, full_kets.ortho_center)
+            k0, k1 = int(offs[held]), int(offs[held + 1])
+            if block == "diag":  # step 0: the held shard is this rank's own (bras)
+                K_dev[nb_lo : nb_lo + len(bras), k0:k1] = overlap_matrix(bras, bras, "train")
+            elif kind == "train" and held < rank:
+                # bra = the lower row index, as compute_gram does (kernel.py:169-175)
+                blk = overlap_matrix(kets, bras, "test")
+                K_dev[k0:k1, nb_lo : nb_lo + len(bras)] = blk
+                K_dev[nb_lo : nb_lo + len(bras), k0:k1] = blk.T
+            else:
+                blk = overlap_matrix(bras, kets, "test")
+                K_dev[nb_lo : nb_lo + len(bras), k0:k1] = blk
+                if kind == "train":
+                    K_dev[k0:k1, nb_lo : nb_lo + len(bras)] = blk.T
+        if t < len(plan) - 1:
+            t0 = time.perf_counter()
+            pad_sites, pad_chi = _ring_shift([pad_sites, pad_chi], rank, world, group)
+            comm += time.perf_counter() - t0
+    return comm
+
+
 def tiles_of(kind: str, chi_cap: int, n_bras: int, n_kets: int, rank: int, world: int) -> tuple:
     """(tiles int32 (T, 2), row_block, col_block) the library assigns to `rank`."""
     lib = N.lib()
@@ -124,6 +261,10 @@ def gram(X_bras, X_kets, cfg, kind: str, budget: float, chi_max: int = 0, group=
             if local is not None and local.chi_cap != cap:
                 local = simulate_rows(X_all[lo:hi], cfg, budget, chi_max, chi_cap=cap)
     rep.n_simulations = n_all
+    mode = _exchange_mode(n_all, local, cap if _exchange(world) else (local.chi_cap if local else 4), cfg, world,
+                          group)
+    if mode == "ring" and world > 1 and min(nb, nk) >= world:
+        return _gram_ring(X_bras, X_kets, cfg, kind, budget, chi_max, group, rank, world, local, cap, t_sim, rep)
     if _exchange(world):
         from .mps import batch_layout
 

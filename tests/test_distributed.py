@@ -78,3 +78,57 @@ def test_shard_partition():
             parts = [shard(n, w, r) for r in range(w)]
             assert parts[0][0] == 0 and parts[-1][1] == n
             assert all(parts[i][1] == parts[i + 1][0] for i in range(w - 1))
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 5, 8])
+def test_ring_plan_covers_every_block_once(world):
+    """Ring exchange (the reference's round-robin, kernel.py:188-266): train
+    computes each unordered shard pair once (own shard as a triangle), test
+    every (bra shard, ket shard) block once."""
+    from paper_2411_09336_b200.distributed import ring_plan
+
+    steps = world // 2 + 1
+    seen = {}
+    for r in range(world):
+        plan = ring_plan(world, r, "train")[:steps]
+        for t, held, block in plan:
+            assert held == (r - t) % world
+            if block is not None:
+                key = frozenset((r, held))
+                seen[key] = seen.get(key, 0) + 1
+                assert (block == "diag") == (held == r)
+    assert len(seen) == world * (world + 1) // 2 and set(seen.values()) == {1}
+    test = [(r, held) for r in range(world) for _, held, b in ring_plan(world, r, "test") if b == "full"]
+    assert sorted(test) == [(r, s) for r in range(world) for s in range(world)]
+
+
+def _ring_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2411_09336_b200.distributed import _ring_shift
+
+        a = torch.full((3, 2), float(rank), dtype=torch.float64)
+        b = torch.full((4,), rank, dtype=torch.int32)
+        for step in range(1, world):
+            a, b = _ring_shift([a, b], rank, world)
+            ok = bool((a == float((rank - step) % world)).all() and (b == (rank - step) % world).all())
+            if not ok:
+                break
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ring_shift_gloo_three_ranks():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ring_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(3)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok in res), res

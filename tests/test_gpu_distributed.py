@@ -21,7 +21,7 @@ def _port():
         return s.getsockname()[1]
 
 
-def _rank(rank, world, port, kind, q):
+def _rank(rank, world, port, kind, q, exchange="allgather"):
     import torch
     import torch.distributed as dist
 
@@ -29,6 +29,9 @@ def _rank(rank, world, port, kind, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2411_09336_b200 as P
+        from paper_2411_09336_b200 import distributed as D
+
+        D.EXCHANGE = exchange
 
         torch.cuda.set_device(0)
         g = golden("headline_m165_d1.npz")
@@ -63,6 +66,40 @@ def test_two_ranks_on_one_gpu_match_single_process(kind):
     K0 = out[0][0]
     assert np.array_equal(K0, ref)
     assert np.abs(K0 - (g["K_train"] if kind == "train" else g["K_test"])).max() < 1e-10
+
+
+@pytest.mark.parametrize("world,kind", [(2, "train"), (3, "train"), (3, "test")])
+def test_ring_exchange_matches_single_process(world, kind):
+    """Ring exchange (each rank keeps its own shard plus one travelling ket
+    shard; for MPS sets beyond HBM) over processes sharing one GPU.  Off-
+    diagonal shard blocks take the lower row index as the bra (the
+    reference's rule) while the single-process train kernel takes the lower
+    position of its ket ordering, so |<a|b>|^2 and |<b|a>|^2 may differ in the
+    last bits: equal to 1e-15, exact unit diagonal and symmetry."""
+    import paper_2411_09336_b200 as P
+
+    g = golden("headline_m165_d1.npz")
+    cfg = P.FeatureMapConfig(165, 2, 1, 0.1)
+    Xb = g["X"] if kind == "train" else g["X_test"]
+    ref = P.run_distributed(Xb, g["X"], cfg, P.make_schedule(len(Xb), len(g["X"]), 1, "round_robin", kind)).entries
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_rank, args=(r, world, port, kind, q, "ring")) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict((r, (K, ns, ni)) for r, K, ns, ni in (q.get(timeout=300) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    K0 = out[0][0]
+    assert np.abs(K0 - ref).max() < 1e-15
+    assert np.abs(K0 - (g["K_train"] if kind == "train" else g["K_test"])).max() < 1e-10
+    if kind == "train":
+        assert np.array_equal(K0, K0.T) and np.all(np.diag(K0) == 1.0)
+    else:
+        assert np.array_equal(K0, ref)  # test blocks: same roles, same tiles
+    assert out[0][2] == (len(g["X"]) * (len(g["X"]) - 1) // 2 if kind == "train" else len(Xb) * len(g["X"]))
 
 
 def _nccl_single(kind, q):
