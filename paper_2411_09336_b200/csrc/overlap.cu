@@ -30,6 +30,9 @@
 #include "internal.h"
 #include "o1_site.cuh"
 
+#ifndef MPSKQ_MMA_GROUP
+#define MPSKQ_MMA_GROUP 0  // warps per pair of the L2-plane DMMA overlap (0: per capacity)
+#endif
 #ifndef MPSKQ_MMA_GLOBAL_CTAS
 #define MPSKQ_MMA_GLOBAL_CTAS 2  // resident CTAs per SM of the L2-plane DMMA overlap
 #endif
@@ -382,6 +385,13 @@ struct MmaCfg {
   static constexpr bool global = max_warps < 8;
   static constexpr int warps = global ? 8 : (max_warps > 16 ? 16 : max_warps);
   static constexpr int ctas_per_sm = global ? MPSKQ_MMA_GLOBAL_CTAS : 1;
+  // warps cooperating on one pair (tiles of each phase split among them):
+  // with L2 planes, 4 per pair keeps the planes in flight (~600 pairs) inside
+  // L2 instead of spilling ~2 TB/s of plane traffic to DRAM
+  // (measured, tools/ov_caps.py: 1 up to capacity 32, 2 at 48/64, 4 from 80:
+  // d=8 71 -> 53 ms, d=7 135 -> 116 ms)
+  static constexpr int gw = !global ? 1 : MPSKQ_MMA_GROUP > 0 ? MPSKQ_MMA_GROUP : CAP <= 32 ? 1 : CAP <= 64 ? 2 : 4;
+  static constexpr int pairs = warps / gw;  // pairs per CTA (ket columns of a tile)
   static constexpr size_t smem = global ? 0 : sizeof(double) * (size_t)per_warp * warps;
 };
 
@@ -424,8 +434,16 @@ __global__ void __launch_bounds__(MmaCfg<CAP>::warps * 32, MmaCfg<CAP>::ctas_per
   extern __shared__ __align__(16) double smem_d[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;  // fragment row group / thread in group
-  double* er = (C::global ? a.gws + ((size_t)blockIdx.x * C::warps) * C::per_warp : smem_d) +
-               (size_t)warp * C::per_warp;
+  const int grp = warp / C::gw, wg = warp % C::gw;  // pair group, warp within it
+  double* er = (C::global ? a.gws + ((size_t)blockIdx.x * C::pairs) * C::per_warp : smem_d) +
+               (size_t)grp * C::per_warp;
+  // the group's warps meet on a named barrier (id 1 + group)
+  auto gsync = [&]() {
+    if constexpr (C::gw > 1)
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(C::gw * 32) : "memory");
+    else
+      __syncwarp();
+  };
   double* ei = er + C::R8 * C::L1;
   double* tr = ei + C::R8 * C::L1;
   double* ti = tr + C::R8 * C::L2;
@@ -434,16 +452,16 @@ __global__ void __launch_bounds__(MmaCfg<CAP>::warps * 32, MmaCfg<CAP>::ctas_per
   for (int64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
     const int2 tile = a.tiles[t];
     const int64_t i = tile.x;
-    const int64_t j = (int64_t)tile.y * C::warps + warp;
-    if (j >= a.n_kets || (train && i >= j)) continue;  // warps are independent
+    const int64_t j = (int64_t)tile.y * C::pairs + grp;
+    if (j >= a.n_kets || (train && i >= j)) continue;  // groups are independent
     const double2* bra = a.bra + i * a.stride;
     const double2* ket = a.ket + j * a.stride;
     const int32_t* bchi = a.bra_chi + i * (m + 1);
     const int32_t* kchi = a.ket_chi + j * (m + 1);
-    for (int idx = lane; idx < 2 * C::R8 * C::L1; idx += 32) er[idx] = 0.0;
-    __syncwarp();
-    if (lane == 0) er[0] = 1.0;  // env = [[1]]
-    __syncwarp();
+    for (int idx = wg * 32 + lane; idx < 2 * C::R8 * C::L1; idx += C::gw * 32) er[idx] = 0.0;
+    gsync();
+    if (wg == 0 && lane == 0) er[0] = 1.0;  // env = [[1]]
+    gsync();
     for (int s = 0; s < m; ++s) {
       const int na = __ldg(bchi + s), na1 = __ldg(bchi + s + 1);
       const int nb = __ldg(kchi + s), nb1 = __ldg(kchi + s + 1);
@@ -453,8 +471,10 @@ __global__ void __launch_bounds__(MmaCfg<CAP>::warps * 32, MmaCfg<CAP>::ctas_per
       {
         const int nt_n = (2 * nb1 + 7) >> 3, mt_n = (na + 7) >> 3, ks_n = (nb + 3) >> 2;
         const int ncol = 2 * nb1;
-        for (int mt = 0; mt < mt_n; ++mt) {
-          for (int nt = 0; nt < nt_n; nt += 2) {
+        const int ntp = (nt_n + 1) >> 1;
+        for (int tt = wg; tt < mt_n * ntp; tt += C::gw) {  // output tile pairs split over the group
+          const int mt = tt / ntp, nt = (tt - mt * ntp) * 2;
+          {
             CTile c0{0, 0, 0, 0}, c1{0, 0, 0, 0};
             const int n0 = nt * 8 + g, n1 = n0 + 8;
             for (int ks = 0; ks < ks_n; ++ks) {
@@ -482,12 +502,14 @@ __global__ void __launch_bounds__(MmaCfg<CAP>::warps * 32, MmaCfg<CAP>::ctas_per
           }
         }
       }
-      __syncwarp();
+      gsync();
       // ---- phase 2: E' (na1 x nb1) = conj(A)^T (na1 x 2na) . T2 (2na x nb1)
       {
         const int nt_n = (nb1 + 7) >> 3, mt_n = (na1 + 7) >> 3, ks_n = (2 * na + 3) >> 2;
-        for (int mt = 0; mt < mt_n; ++mt) {
-          for (int nt = 0; nt < nt_n; nt += 2) {
+        const int ntp = (nt_n + 1) >> 1;
+        for (int tt = wg; tt < mt_n * ntp; tt += C::gw) {
+          const int mt = tt / ntp, nt = (tt - mt * ntp) * 2;
+          {
             CTile c0{0, 0, 0, 0}, c1{0, 0, 0, 0};
             const int ar_ = mt * 8 + g;
             const int n0 = nt * 8 + g, n1 = n0 + 8;
@@ -524,10 +546,10 @@ __global__ void __launch_bounds__(MmaCfg<CAP>::warps * 32, MmaCfg<CAP>::ctas_per
           }
         }
       }
-      __syncwarp();
+      gsync();
     }
-    if (lane == 0) store_result(a.out_mode, a.out, a.ld, i, j, make_double2(er[0], ei[0]), train);
-    __syncwarp();
+    if (wg == 0 && lane == 0) store_result(a.out_mode, a.out, a.ld, i, j, make_double2(er[0], ei[0]), train);
+    gsync();
   }
 }
 
@@ -702,7 +724,7 @@ int launch_mma(const OverlapArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(mma)");
   }
   const bool train = a.kind == MPSKQ_KIND_TRAIN;
-  auto tiles = make_tiles(train, a.n_bras, a.n_kets, 1, C::warps, a.rank, a.world);
+  auto tiles = make_tiles(train, a.n_bras, a.n_kets, 1, C::pairs, a.rank, a.world);
   int2* dtiles = nullptr;
   if (int s = upload_tiles(tiles, &dtiles, st)) return s;
   if (!tiles.empty()) {
@@ -728,7 +750,7 @@ int launch_mma(const OverlapArgs& a, cudaStream_t st) {
     const int grid = (int)std::min<int64_t>((int64_t)tiles.size(), (int64_t)sms * (C::global ? 2 * C::ctas_per_sm : 16));
     if (C::global) {
       e = cudaMallocAsync(reinterpret_cast<void**>(&o.gws),
-                          sizeof(double) * (size_t)C::per_warp * C::warps * grid, st);
+                          sizeof(double) * (size_t)C::per_warp * C::pairs * grid, st);
       if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(mma planes)");
     }
     overlap_mma_kernel<CAP><<<grid, C::warps * 32, C::smem, st>>>(o);
@@ -773,16 +795,16 @@ int launch_overlap(const OverlapArgs& a, void* stream) {
 void tile_shape(int chi_cap, int* rb, int* cb) {
   switch (chi_cap) {
     case 4: *rb = kWarpsO1; *cb = kLanes; return;
-    case 8: *rb = 1; *cb = MmaCfg<8>::warps; return;
-    case 12: *rb = 1; *cb = MmaCfg<12>::warps; return;
-    case 16: *rb = 1; *cb = MmaCfg<16>::warps; return;
-    case 24: *rb = 1; *cb = MmaCfg<24>::warps; return;
-    case 32: *rb = 1; *cb = MmaCfg<32>::warps; return;
-    case 48: *rb = 1; *cb = MmaCfg<48>::warps; return;
-    case 64: *rb = 1; *cb = MmaCfg<64>::warps; return;
-    case 80: *rb = 1; *cb = MmaCfg<80>::warps; return;
-    case 96: *rb = 1; *cb = MmaCfg<96>::warps; return;
-    default: *rb = 1; *cb = MmaCfg<128>::warps; return;
+    case 8: *rb = 1; *cb = MmaCfg<8>::pairs; return;
+    case 12: *rb = 1; *cb = MmaCfg<12>::pairs; return;
+    case 16: *rb = 1; *cb = MmaCfg<16>::pairs; return;
+    case 24: *rb = 1; *cb = MmaCfg<24>::pairs; return;
+    case 32: *rb = 1; *cb = MmaCfg<32>::pairs; return;
+    case 48: *rb = 1; *cb = MmaCfg<48>::pairs; return;
+    case 64: *rb = 1; *cb = MmaCfg<64>::pairs; return;
+    case 80: *rb = 1; *cb = MmaCfg<80>::pairs; return;
+    case 96: *rb = 1; *cb = MmaCfg<96>::pairs; return;
+    default: *rb = 1; *cb = MmaCfg<128>::pairs; return;
   }
 }
 
