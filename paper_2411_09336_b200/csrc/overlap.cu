@@ -246,12 +246,13 @@ struct O1Args {
 
 // One CTA = 8 bras (warps) x 32 kets (lanes); one thread owns one pair's 4x4
 // complex environment in registers.  Persistent over its tiles, the CTA
-// streams each site's ket block (16 KB) and bra tile (4 KB) into a 6-stage
+// streams each site's ket block (16 KB) and bra tile (4 KB) into an 8-stage
 // shared-memory ring with TMA bulk copies (cp.async.bulk) completing on
 // "full" mbarriers; every warp releases a slot on its "empty" mbarrier, so
 // warps drift up to the ring depth instead of synchronising every site.
-// Thread 0 is the producer: it refills opportunistically (test_wait) and
-// blocks only for the slot its own warp needs next (deadlock free).
+// Every warp can produce (lane 0 issues, the warp decides collectively): it
+// refills free slots opportunistically (test_wait) and blocks only for the
+// slot it needs next, so the fastest warp keeps the ring full (deadlock free).
 __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* sket = reinterpret_cast<double2*>(smem_raw);
