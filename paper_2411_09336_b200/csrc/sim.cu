@@ -31,6 +31,33 @@ __device__ constexpr double kNoiseFloor = 10.0 * DBL_EPSILON;
 // 1/sqrt(2) exactly as the reference rounds it: _H_MATRIX = [[1,1],[1,-1]]/sqrt(2)
 __device__ constexpr double kInvSqrt2 = 0.7071067811865475;
 constexpr int kMaxSweeps = 40;
+// Lanes (threads) per state by capacity.  Same-box A/B of the simulator
+// (tools/ab_sim_headline.py, tools/ab_sim_cfg.py, tools/ab_sim.py): halving
+// the old 16/64/128/256/384 sped up capacity 4 (15.6 -> 13.7 ms at the
+// headline), 8 (34 -> 30 ms), 12-16 (28 -> 23 ms), 24-32 (1.84 -> 1.57 s) and
+// 48 (-3%); halving again was slower except at 12-16, and 4 lanes breaks the
+// capacity-4 Jacobi.  Capacities >= 64 keep 512.
+#ifndef MPSKQ_NT4
+#define MPSKQ_NT4 8
+#endif
+#ifndef MPSKQ_NT8
+#define MPSKQ_NT8 32
+#endif
+#ifndef MPSKQ_NT16
+#define MPSKQ_NT16 32
+#endif
+#ifndef MPSKQ_NT32
+#define MPSKQ_NT32 128
+#endif
+#ifndef MPSKQ_NT48
+#define MPSKQ_NT48 192
+#endif
+#ifndef MPSKQ_NT128
+#define MPSKQ_NT128 512
+#endif
+#ifndef MPSKQ_SPC_THREADS
+#define MPSKQ_SPC_THREADS 128  // threads of a lockstepped multi-state CTA (NT <= 32)
+#endif
 // QR preconditioning of the two-qubit SVD from this many columns up (below it
 // the direct Jacobi needs only ~3 sweeps and the QR would not pay)
 constexpr int kPrecondMinCols = 8;
@@ -72,7 +99,7 @@ __device__ __forceinline__ int ltid() {
 template <int CAP>
 struct NtFor {
   static constexpr int value =
-      CAP <= 4 ? 16 : CAP <= 8 ? 64 : CAP <= 16 ? 128 : CAP <= 32 ? 256 : CAP <= 48 ? 384 : 512;
+      CAP <= 4 ? MPSKQ_NT4 : CAP <= 8 ? MPSKQ_NT8 : CAP <= 16 ? MPSKQ_NT16 : CAP <= 32 ? MPSKQ_NT32 : CAP <= 48 ? MPSKQ_NT48 : MPSKQ_NT128;
 };
 
 // Capacities above 48: theta/C and the staging buffer no longer fit shared
@@ -665,8 +692,8 @@ template <int CAP, int NT>
 __device__ int jacobi(Smem<CAP, NT>& sm, int Rr, int n) {
   if constexpr (!LogW<CAP>::value) init_identity<CAP, NT>(sm.W, n);
   if (n < 2) return 0;
-  // lanes per column pair: G * (n/2) <= NT, G in {4, 8, 16, 32} for every
-  // (CAP, NT) instantiation (NT >= 4 * CAP)
+  // lanes per column pair: G * (n/2) <= NT, G in {2, 4, 8, 16, 32} for every
+  // (CAP, NT) instantiation (NT >= 2 * CAP)
   const int G = group_width<NT>((n + 1) >> 1);
   if (G >= 32) return jacobi_sweeps<CAP, NT, 32>(sm, Rr, n);
   if (G == 16) return jacobi_sweeps<CAP, NT, 16>(sm, Rr, n);
@@ -1049,7 +1076,7 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
 // region of the (large) op code and the instruction cache keeps up.
 template <int NT>
 struct SpcFor {
-  static constexpr int value = NT <= 32 ? 128 / NT : 1;
+  static constexpr int value = NT <= 32 ? MPSKQ_SPC_THREADS / NT : 1;
 };
 
 template <int CAP, int NT>
