@@ -105,20 +105,26 @@ struct NtFor {
 // Capacities above 48: theta/C and the staging buffer no longer fit shared
 // memory; they live in a per-CTA global scratch (L2 resident), the small
 // per-op arrays stay in shared memory.
+// At capacity 64 W gets its own plane there too and is accumulated during
+// the Jacobi (no rotation log, no replay): d=7 sim 6.34 -> 5.48 s.  At 96 and
+// 128 the same change measured neutral / +2% (the per-round W rotation over
+// 2*CAP rows costs what the replay saved), so they keep the log.
 template <int CAP>
 struct GlobalWs {
   static constexpr bool value = CAP > 48;
-  static constexpr int64_t complexes = (int64_t)(2 * CAP) * (2 * CAP) + 2 * (int64_t)CAP * CAP;
+  static constexpr bool direct_w = value && CAP <= 64;
+  static constexpr int64_t complexes =
+      (direct_w ? 2 : 1) * (int64_t)(2 * CAP) * (2 * CAP) + 2 * (int64_t)CAP * CAP;
 };
 
-// Capacities above 32 keep only theta/C in shared memory: the Jacobi rotations
-// are logged to a per-CTA global buffer and replayed on the identity after
-// the C-side factor has been written out (W then reuses C's space).  (Using it
-// from capacity 12 up doubles the resident states but the replay costs about
-// as much as it saves: measured neutral to negative.)
+// Capacities 48 and 80-128 keep only theta/C on the fast side: the Jacobi
+// rotations are logged to a per-CTA global buffer and replayed on the identity
+// after the C-side factor has been written out (W then reuses C's space).
+// (Using it from capacity 12 up doubles the resident states but the replay
+// costs about as much as it saves: measured neutral to negative.)
 template <int CAP>
 struct LogW {
-  static constexpr bool value = CAP > 32;
+  static constexpr bool value = CAP > 32 && !GlobalWs<CAP>::direct_w;
   static constexpr int64_t entries = (int64_t)kMaxSweeps * (2 * CAP) * CAP;  // sweeps x rounds x pairs
 };
 
@@ -155,7 +161,7 @@ struct Smem {
     if constexpr (GlobalWs<CAP>::value) {
       A = gws;
       S = gws + LD * LD;
-      W = S;
+      W = GlobalWs<CAP>::direct_w ? S + 2 * CAP * CAP : S;
     } else {
       A = reinterpret_cast<double2*>(p);
       p += sizeof(double2) * LD * LD;
@@ -1088,7 +1094,7 @@ __global__ void __launch_bounds__(NT * SpcFor<NT>::value) sim_kernel(SimArgs a) 
   double2* gws = nullptr;
   if constexpr (GlobalWs<CAP>::value)
     gws = reinterpret_cast<double2*>(static_cast<double4*>(a.scratch) +
-                                     (int64_t)gridDim.x * LogW<CAP>::entries) +
+                                     (LogW<CAP>::value ? (int64_t)gridDim.x * LogW<CAP>::entries : 0)) +
           (int64_t)blockIdx.x * GlobalWs<CAP>::complexes;
   sm.carve(smem_raw + (size_t)slot * Smem<CAP, NT>::bytes(a.m), a.m, gws);
   if constexpr (LogW<CAP>::value)
@@ -1172,7 +1178,7 @@ __global__ void __launch_bounds__(NT) svd_kernel(SvdArgs a) {
   double2* gws = nullptr;
   if constexpr (GlobalWs<CAP>::value)
     gws = reinterpret_cast<double2*>(static_cast<double4*>(a.scratch) +
-                                     (int64_t)gridDim.x * LogW<CAP>::entries) +
+                                     (LogW<CAP>::value ? (int64_t)gridDim.x * LogW<CAP>::entries : 0)) +
           (int64_t)blockIdx.x * GlobalWs<CAP>::complexes;
   sm.carve(smem_raw, 0, gws);
   if constexpr (LogW<CAP>::value)
@@ -1249,8 +1255,8 @@ template <int CAP, class K>
 int plan_grid(K kernel, int threads, size_t smem, int64_t items, cudaStream_t st, int64_t* grid, void** scratch) {
   *grid = items < (int64_t(1) << 30) ? items : (int64_t(1) << 30);
   *scratch = nullptr;
-  if constexpr (LogW<CAP>::value) {
-    // persistent grid of all co-resident CTAs, each with its own log slice
+  if constexpr (LogW<CAP>::value || GlobalWs<CAP>::value) {
+    // persistent grid of all co-resident CTAs, each with its own log slice / workspace
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1259,7 +1265,7 @@ int plan_grid(K kernel, int threads, size_t smem, int64_t items, cudaStream_t st
       per_sm = 1;
     const int64_t cap = (int64_t)sms * per_sm;
     *grid = items < cap ? items : cap;
-    size_t bytes = sizeof(double4) * LogW<CAP>::entries * *grid;
+    size_t bytes = LogW<CAP>::value ? sizeof(double4) * LogW<CAP>::entries * *grid : 0;
     if constexpr (GlobalWs<CAP>::value) bytes += sizeof(double2) * GlobalWs<CAP>::complexes * *grid;
     cudaError_t e = cudaMallocAsync(scratch, bytes, st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(rotation log)");

@@ -263,6 +263,12 @@ if __name__ == "__main__" and "--large-chi" in sys.argv:
     gram_case("config5_m100_d8", 100, 2, 8, 0.1, 1e-16, 4, 2, seed=0)
 
 
+if __name__ == "__main__" and "--d7" in sys.argv:
+    # config 5 at d=7: peak chi 49-64, i.e. the capacity-64 path (theta and W
+    # in the global workspace, no rotation log)
+    gram_case("config5_m100_d7", 100, 2, 7, 0.1, 1e-16, 4, 2, seed=0)
+
+
 def svd_cases_large():
     """svd_truncated on 65..96-sized matrices (the capacity-48 device path)."""
     rng = np.random.default_rng(77)

@@ -364,6 +364,32 @@ def test_large_chi_global_workspace_path():
     assert np.abs(Kt - g["K_test"]).max() < 1e-6
 
 
+def test_capacity_64_direct_w_path():
+    """Config 5 at d=7 (m=100, budget 1e-16) peaks at chi 50-51 on these rows:
+    capacity 64 keeps theta and the Jacobi W in the global workspace and
+    accumulates W in place (no rotation log).  Same bond dims and peaks as the
+    reference; the same rows through capacity 80 (rotation log) agree too."""
+    import paper_2411_09336_b200 as P
+    from paper_2411_09336_b200.kernel import simulate_rows
+
+    g = golden("config5_m100_d7.npz")
+    cfg, budget = _cfg(g)
+    tr = P.simulate_dataset(g["X"], cfg, budget=budget)
+    te = P.simulate_dataset(g["X_test"], cfg, budget=budget)
+    assert tr.chi_cap == 64 and te.chi_cap == 64
+    assert np.array_equal(tr.bond_dims(), g["train_chi"])
+    assert np.array_equal(te.bond_dims(), g["test_chi"])
+    assert np.array_equal(tr.peak.cpu().numpy(), g["train_peak"])
+    assert np.array_equal(te.peak.cpu().numpy(), g["test_peak"])
+    K = P.compute_gram(tr, tr, "train").entries
+    Kt = P.compute_gram(te, tr, "test").entries
+    assert np.abs(K - g["K_train"]).max() < 1e-6
+    assert np.abs(Kt - g["K_test"]).max() < 1e-6
+    b80 = simulate_rows(g["X"], cfg, budget, chi_cap=80)
+    assert b80.chi_cap == 80 and np.array_equal(b80.bond_dims(), g["train_chi"])
+    assert np.abs(P.compute_gram(b80, b80, "train").entries - g["K_train"]).max() < 1e-6
+
+
 def test_svd_truncated_large_matrices():
     import paper_2411_09336_b200 as P
 
