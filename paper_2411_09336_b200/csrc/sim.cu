@@ -139,7 +139,9 @@ struct Smem {
   double2* ud;   // LD: diagonal entries of the pivoted QR's reflectors
   double* tau;   // LD
   double* sig;   // LD
-  double* red;   // 32
+  double* red;   // kRed
+  static constexpr int kRedHalf = NT / 32 > 16 ? NT / 32 : 16;  // warps of the group (>= 16)
+  static constexpr int kRed = 2 * kRedHalf;
   double* scal;  // 4: factor, discarded
   int* perm;     // LD
   int* piv;      // LD: inverse column order of the pivoted QR
@@ -151,7 +153,7 @@ struct Smem {
     size_t b = GlobalWs<CAP>::value
                    ? sizeof(double2) * 2 * LD
                    : sizeof(double2) * ((LogW<CAP>::value ? 1 : 2) * LD * LD + 2 * CAP * CAP + 2 * LD);
-    b += sizeof(double) * (2 * LD + 32 + 4);
+    b += sizeof(double) * (2 * LD + kRed + 4);
     b += sizeof(int) * (2 * LD + 4 + m + 1);
     return (b + 15) & ~size_t(15);
   }
@@ -182,7 +184,7 @@ struct Smem {
     sig = reinterpret_cast<double*>(p);
     p += sizeof(double) * LD;
     red = reinterpret_cast<double*>(p);
-    p += sizeof(double) * 32;
+    p += sizeof(double) * kRed;
     scal = reinterpret_cast<double*>(p);
     p += sizeof(double) * 4;
     perm = reinterpret_cast<int*>(p);
@@ -290,7 +292,7 @@ __device__ __forceinline__ double2 r_entry(const Smem<CAP, NT>& sm, int kk, int 
 // so the scaled side is P Z (rows permuted) and the orthonormal side Q W'
 // (reflectors applied to W'), the same roles C W and W play unpreconditioned.
 
-// group-wide argmax of (v, idx), ties to the smaller idx; `red` needs 32 doubles
+// group-wide argmax of (v, idx), ties to the smaller idx; `red` needs Smem::kRed doubles
 template <int NT>
 __device__ __forceinline__ int block_argmax(double v, int idx, double* red) {
   const unsigned mask = group_mask<NT>();
@@ -305,20 +307,20 @@ __device__ __forceinline__ int block_argmax(double v, int idx, double* red) {
     }
   }
   if constexpr (NT > 32) {
-    static_assert(NT <= 512, "red holds 16 warps");
+    constexpr int H = NT / 32 > 16 ? NT / 32 : 16;  // Smem::kRedHalf
     const int w = threadIdx.x >> 5;
     __syncthreads();
     if ((threadIdx.x & 31) == 0) {
       red[w] = v;
-      red[16 + w] = (double)idx;
+      red[H + w] = (double)idx;
     }
     __syncthreads();
     v = red[0];
-    idx = (int)red[16];
+    idx = (int)red[H];
 #pragma unroll
     for (int i = 1; i < NT / 32; ++i) {
       const double ov = red[i];
-      const int oi = (int)red[16 + i];
+      const int oi = (int)red[H + i];
       if (ov > v || (ov == v && oi < idx)) {
         v = ov;
         idx = oi;
