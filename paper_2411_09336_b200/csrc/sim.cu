@@ -109,10 +109,13 @@ struct NtFor {
 // the Jacobi (no rotation log, no replay): d=7 sim 6.34 -> 5.48 s.  At 96 and
 // 128 the same change measured neutral / +2% (the per-round W rotation over
 // 2*CAP rows costs what the replay saved), so they keep the log.
+#ifndef MPSKQ_DIRECT_W_MAX
+#define MPSKQ_DIRECT_W_MAX 64  // A/B knob
+#endif
 template <int CAP>
 struct GlobalWs {
   static constexpr bool value = CAP > 48;
-  static constexpr bool direct_w = value && CAP <= 64;
+  static constexpr bool direct_w = value && CAP <= MPSKQ_DIRECT_W_MAX;
   static constexpr int64_t complexes =
       (direct_w ? 2 : 1) * (int64_t)(2 * CAP) * (2 * CAP) + 2 * (int64_t)CAP * CAP;
 };
