@@ -372,7 +372,9 @@ def gpu_main(args) -> None:
         wall_ms = 1e3 * (time.perf_counter() - w0) / args.steps
         e2e = {"value": n * (n - 1) / 2 / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": X.nbytes,
                "d2h_bytes_per_step": n * n * 8, "ms_per_step": e2e_ms, "host_wall_ms_per_step": wall_ms,
-               "path": "C ABI mpskq_gram_host (pinned host rows -> pinned host K)"}
+               "path": "C ABI mpskq_gram_host (pinned host rows -> pinned host K, row bands streamed "
+                       "to host under the overlap)",
+               "k_bitwise_equal_device_path": bool(torch.equal(Kp, K.cpu()))}
     else:
         sched = P.make_schedule(n, n, world, "round_robin", "train")
         for _ in range(max(1, args.warmup)):

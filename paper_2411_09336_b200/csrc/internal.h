@@ -80,6 +80,11 @@ struct OverlapArgs {
   int rank, world;
   double* out;
   int64_t ld;
+  // optional: pinned, device-mapped host K (train/test kernel values, chi <= 4
+  // path, one rank).  The overlap then runs one launch per super-row of bra
+  // tiles and a side stream writes each finished row band straight into host
+  // memory while the next band computes; `out` is not touched.
+  double* host_out = nullptr;
 };
 int launch_overlap(const OverlapArgs& a, void* stream);
 

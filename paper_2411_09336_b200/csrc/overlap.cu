@@ -184,6 +184,23 @@ __global__ void unpermute_kernel(const T* __restrict__ ordered, int64_t nk, cons
   }
 }
 
+// Host-streaming variant for one band of ordered rows [r0, r1): caller row
+// a = row_of[o] (train; identity for test bras) is gathered like
+// unpermute_kernel and written straight into pinned host memory (one
+// contiguous row per CTA pass, coalesced over the link); the train diagonal
+// is written here as 1.0 (compute_gram's eye, kernel.py:168).
+__global__ void rows_to_host_kernel(const double* __restrict__ ordered, int64_t nk,
+                                    const int32_t* __restrict__ row_of, int64_t r0, int64_t r1,
+                                    const int32_t* __restrict__ kpos, bool train,
+                                    double* __restrict__ out, int64_t ld) {
+  for (int64_t o = r0 + blockIdx.x; o < r1; o += gridDim.x) {
+    const int64_t a = row_of ? row_of[o] : o;
+    const double* row = ordered + o * nk;
+    for (int64_t b = threadIdx.x; b < nk; b += blockDim.x)
+      out[a * ld + b] = (train && b == a) ? 1.0 : row[kpos[b]];
+  }
+}
+
 __device__ __forceinline__ void store_result(int out_mode, double* out, int64_t ld, int64_t i,
                                              int64_t j, double2 ov, bool mirror) {
   if (out_mode == MPSKQ_OUT_KERNEL) {
@@ -576,17 +593,22 @@ int upload_tiles(const std::vector<int2>& tiles, int2** dev, cudaStream_t st) {
 // super-block (about 384 bras x 384 kets each) so the tiles that run
 // concurrently on the 148 SMs share their bra and ket site data in L2.
 // Block-cyclic over ranks: tile t goes to rank t % world.
+inline int64_t super_rows(int rb) { return std::max<int64_t>(1, 384 / rb); }
+
+// [i_lo, i_hi): row-block range (the host-streaming path enumerates one
+// super-row at a time; the default covers every row block)
 std::vector<int2> make_tiles(bool train, int64_t n_rows, int64_t n_cols, int rb, int cb, int rank,
-                             int world) {
+                             int world, int64_t i_lo = 0, int64_t i_hi = -1) {
   std::vector<int2> tiles;
   const int64_t nrb = (n_rows + rb - 1) / rb, ncb = (n_cols + cb - 1) / cb;
-  const int64_t sr = std::max<int64_t>(1, 384 / rb), sc = std::max<int64_t>(1, 384 / cb);
+  const int64_t sr = super_rows(rb), sc = std::max<int64_t>(1, 384 / cb);
+  const int64_t ihi = i_hi < 0 ? nrb : std::min(nrb, i_hi);
   int64_t t = 0;
   for (int64_t J0 = 0; J0 < ncb; J0 += sc) {
-    for (int64_t I0 = 0; I0 < nrb; I0 += sr) {
+    for (int64_t I0 = i_lo; I0 < ihi; I0 += sr) {
       for (int64_t J = J0; J < std::min(ncb, J0 + sc); ++J) {
         const int64_t jmax = std::min(n_cols, (J + 1) * cb) - 1;
-        for (int64_t I = I0; I < std::min(nrb, I0 + sr); ++I) {
+        for (int64_t I = I0; I < std::min(ihi, I0 + sr); ++I) {
           if (train && I * rb >= jmax) break;
           if (t++ % world == rank) tiles.push_back(make_int2((int)I, (int)J));
         }
@@ -674,7 +696,23 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
   pack_o1_kernel<<<blocks_for((int64_t)m * nbk * kEnt * kLanes), threads, 0, st>>>(
       reinterpret_cast<const double2*>(a.ket_sites), a.ket_chi, a.site_off, a.state_stride, m,
       a.n_kets, nbk, kperm, static_cast<double2*>(ket));
-  auto tiles = make_tiles(train, a.n_bras, a.n_kets, kWarpsO1, kLanes, a.rank, a.world);
+  // host streaming: one tile list per super-row band, concatenated
+  const bool to_host = a.host_out != nullptr && a.out_mode == MPSKQ_OUT_KERNEL && a.world == 1;
+  std::vector<int64_t> band_rows{0}, band_tiles{0};  // band b: ordered rows / tiles [b], [b+1]
+  std::vector<int2> tiles;
+  if (to_host) {
+    const int64_t nrb = npb / kWarpsO1, sr = super_rows(kWarpsO1);
+    for (int64_t I0 = 0; I0 < nrb; I0 += sr) {
+      auto t = make_tiles(train, a.n_bras, a.n_kets, kWarpsO1, kLanes, 0, 1, I0, I0 + sr);
+      tiles.insert(tiles.end(), t.begin(), t.end());
+      band_rows.push_back(std::min<int64_t>(a.n_bras, (I0 + sr) * kWarpsO1));
+      band_tiles.push_back((int64_t)tiles.size());
+    }
+  } else {
+    tiles = make_tiles(train, a.n_bras, a.n_kets, kWarpsO1, kLanes, a.rank, a.world);
+    band_rows.push_back(a.n_bras);
+    band_tiles.push_back((int64_t)tiles.size());
+  }
   int2* dtiles = nullptr;
   if ((s_ = upload_tiles(tiles, &dtiles, st))) {
     release();
@@ -682,7 +720,58 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
   }
   frees.push_back(dtiles);
   cudaError_t e = cudaSuccess;
-  if (!tiles.empty()) {
+  if (to_host) {
+    const size_t smem = o1_smem_bytes(m);
+    e = cudaFuncSetAttribute(overlap_o1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+      release();
+      return cuda_fail(e, "cudaFuncSetAttribute(o1)");
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaStream_t side = nullptr;
+    e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      release();
+      return cuda_fail(e, "cudaStreamCreate(side)");
+    }
+    const int32_t* row_of = train ? kperm : nullptr;
+    const int bands = (int)band_rows.size() - 1;
+    for (int b = 0; b < bands && e == cudaSuccess; ++b) {
+      const int64_t nt = band_tiles[b + 1] - band_tiles[b];
+      if (nt > 0) {
+        O1Args o{static_cast<const double2*>(bra), static_cast<const double2*>(ket), a.bra_chi,
+                 a.n_bras, a.n_kets, npb, nbk, m, a.kind,
+                 a.out_mode, dtiles + band_tiles[b], nt, static_cast<double*>(ordered), a.n_kets,
+                 bperm, kperm, static_cast<const uint8_t*>(narrow)};
+        overlap_o1_kernel<<<(int)std::min<int64_t>(nt, sms), kWarpsO1 * 32, smem, st>>>(o);
+      }
+      // rows of this band are final once its tiles ran (mirrored entries of
+      // train only ever land in later rows): hand the band to the side stream
+      cudaEvent_t ev;
+      if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) break;
+      cudaEventRecord(ev, st);
+      cudaStreamWaitEvent(side, ev, 0);
+      cudaEventDestroy(ev);
+      const int64_t r0 = band_rows[b], r1 = band_rows[b + 1];
+      if (r1 > r0)
+        rows_to_host_kernel<<<(int)std::min<int64_t>(r1 - r0, 296), 256, 0, side>>>(
+            static_cast<const double*>(ordered), a.n_kets, row_of, r0, r1,
+            static_cast<const int32_t*>(kinv), train, a.host_out, a.ld);
+      e = cudaGetLastError();
+    }
+    // join: the main stream (and the buffer frees below) wait for the last band
+    cudaEvent_t done;
+    if (cudaEventCreateWithFlags(&done, cudaEventDisableTiming) == cudaSuccess) {
+      cudaEventRecord(done, side);
+      cudaStreamWaitEvent(st, done, 0);
+      cudaEventDestroy(done);
+    } else {
+      cudaStreamSynchronize(side);
+    }
+    cudaStreamDestroy(side);
+  } else if (!tiles.empty()) {
     const size_t smem = o1_smem_bytes(m);
     e = cudaFuncSetAttribute(overlap_o1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
@@ -784,7 +873,8 @@ int launch_overlap(const OverlapArgs& a, void* stream) {
     default: return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", a.chi_cap);
   }
   if (s != MPSKQ_OK) return s;
-  if (a.kind == MPSKQ_KIND_TRAIN && a.out_mode == MPSKQ_OUT_KERNEL && a.rank == 0) {
+  if (a.kind == MPSKQ_KIND_TRAIN && a.out_mode == MPSKQ_OUT_KERNEL && a.rank == 0 &&
+      !(a.host_out && a.chi_cap == 4 && a.world == 1)) {
     fill_diag_kernel<<<(int)std::min<int64_t>((a.n_bras + 255) / 256, 1024), 256, 0, st>>>(
         a.out, a.ld, a.n_bras);
     cudaError_t e = cudaGetLastError();

@@ -598,17 +598,38 @@ extern "C" int mpskq_gram_host(int kind, int m, int r, int d, double gamma, doub
   }
   CK(cudaEventRecord(ev[1], st));
 
-  AsyncBuf dK;
-  ST(dK.alloc(sizeof(double) * n_bras * n_kets, st));
   const double* bra_sites = sites.as<double>();
   const int32_t* bra_chi = chi.as<int32_t>();
   const double* ket_sites = train ? bra_sites : bra_sites + 2 * stride * n_bras;
   const int32_t* ket_chi = train ? bra_chi : bra_chi + (m + 1) * n_bras;
-  ST(mpskq_overlap(kind, MPSKQ_OUT_KERNEL, m, cap, doff.as<int64_t>(), stride, bra_sites, bra_chi,
-                   n_bras, ket_sites, ket_chi, n_kets, 0, 1, dK.as<double>(), n_kets, stream));
-  CK(cudaEventRecord(ev[2], st));
-  if (n_bras * n_kets)
-    CK(cudaMemcpyAsync(K_out, dK.p, sizeof(double) * n_bras * n_kets, cudaMemcpyDeviceToHost, st));
+  // Pinned (page-locked, device-mapped) K_out on the chi <= 4 path: the
+  // overlap streams finished row bands straight into it while later bands
+  // compute, so the 8 B/entry device->host transfer hides under the overlap.
+  // Pageable K_out: device K, then one copy.
+  double* k_mapped = nullptr;
+  if (cap == 4 && n_bras > 0 && n_kets > 0) {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, K_out) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer)
+      k_mapped = static_cast<double*>(pa.devicePointer);
+    cudaGetLastError();  // a pageable pointer may leave a sticky-free error behind
+  }
+  AsyncBuf dK;
+  if (k_mapped) {
+    OverlapArgs a{kind,      MPSKQ_OUT_KERNEL, m,      cap,       doff.as<int64_t>(), stride,
+                  bra_sites, bra_chi,          n_bras, ket_sites, ket_chi,            n_kets,
+                  0,         1,                nullptr, n_kets};
+    a.host_out = k_mapped;
+    ST(launch_overlap(a, stream));
+    CK(cudaEventRecord(ev[2], st));
+  } else {
+    ST(dK.alloc(sizeof(double) * n_bras * n_kets, st));
+    ST(mpskq_overlap(kind, MPSKQ_OUT_KERNEL, m, cap, doff.as<int64_t>(), stride, bra_sites, bra_chi,
+                     n_bras, ket_sites, ket_chi, n_kets, 0, 1, dK.as<double>(), n_kets, stream));
+    CK(cudaEventRecord(ev[2], st));
+    if (n_bras * n_kets)
+      CK(cudaMemcpyAsync(K_out, dK.p, sizeof(double) * n_bras * n_kets, cudaMemcpyDeviceToHost, st));
+  }
   CK(cudaEventRecord(ev[3], st));
   CK(cudaStreamSynchronize(st));
   if (seconds) {

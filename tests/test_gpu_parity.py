@@ -456,3 +456,37 @@ def test_largest_capacities_match_reference(cap):
     assert np.array_equal(b.peak.cpu().numpy(), g["train_peak"])
     K = P.compute_gram(b, b, "train").entries
     assert np.abs(K - g["K_train"]).max() < 1e-6
+
+
+def test_c_abi_end_to_end_pinned_output_streams_bitwise(native):
+    """mpskq_gram_host with a pinned K: the chi <= 4 overlap streams finished
+    row bands into host memory (several 384-row bands here) — bitwise equal
+    to the pageable path (device K + one copy), train diagonal exactly 1."""
+    import torch
+
+    from paper_2411_09336_b200 import _native as N
+
+    rng = np.random.default_rng(7)
+    m, r, d, gamma, budget = 165, 2, 1, 0.1, 1e-24
+    X = np.ascontiguousarray(rng.uniform(0, 2, (900, m)))
+    Xt = np.ascontiguousarray(rng.uniform(0, 2, (500, m)))
+
+    def call(kind, bras, kets, out):
+        n_k = bras.shape[0] if kets is None else kets.shape[0]
+        assert out.shape == (bras.shape[0], n_k)
+        N.check(native.mpskq_gram_host(kind, m, r, d, gamma, budget, 0, 4, N.ptr(bras, C.c_double),
+                                       bras.shape[0], None if kets is None else N.ptr(kets, C.c_double),
+                                       0 if kets is None else kets.shape[0],
+                                       C.cast(out.ctypes.data if isinstance(out, np.ndarray) else out.data_ptr(),
+                                              C.POINTER(C.c_double)), None, None))
+        return out
+
+    for kind, bras, kets in ((N.KIND_TRAIN, X, None), (N.KIND_TEST, Xt, X)):
+        shape = (bras.shape[0], X.shape[0])
+        ref = call(kind, bras, kets, np.zeros(shape))
+        pinned = torch.full(shape, -7.0, dtype=torch.float64).pin_memory()
+        got = call(kind, bras, kets, pinned).numpy()
+        assert np.array_equal(got, ref)
+        if kind == N.KIND_TRAIN:
+            assert np.array_equal(np.diag(got), np.ones(shape[0]))
+            assert np.array_equal(got, got.T)
