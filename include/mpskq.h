@@ -186,7 +186,11 @@ int mpskq_overlap_tiles(int kind, int chi_cap, int64_t n_bras, int64_t n_kets, i
  * (train rows).  chi_cap = 0 picks the smallest compiled capacity that
  * holds the result (retrying on MPSKQ_STATE_CAPACITY).  seconds (nullable,
  * 4 doubles) receives {simulation, inner_products, communication, merge}
- * device times (RunReport.seconds keys, kernel.py:100-107).                 */
+ * device times (RunReport.seconds keys, kernel.py:100-107).  A page-locked
+ * K_out (cudaHostAlloc / torch pin_memory) on the chi <= 4 path receives K
+ * band by band while the overlap still runs (the copy then sits inside
+ * "inner_products" and "merge" is ~0); a pageable K_out gets one copy at the
+ * end.  The values are bitwise the same either way.                       */
 int mpskq_gram_host(int kind, int m, int r, int d, double gamma, double budget, int chi_max,
                     int chi_cap, const double* X_bras, int64_t n_bras, const double* X_kets,
                     int64_t n_kets, double* K_out, void* stream, double* seconds);
