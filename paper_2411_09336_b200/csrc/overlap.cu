@@ -730,30 +730,42 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaStream_t side = nullptr;
-    e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+    // Bands alternate between two streams so band b+1's CTAs take the SMs
+    // that band b's tail frees (no idle tail per launch).  Band b's rows are
+    // final once bands <= b ran (train mirrors only write into later rows),
+    // i.e. after the events of b and b-1 (each stream is ordered); the side
+    // stream then writes them to the host.
+    cudaStream_t side = nullptr, alt = nullptr;
+    if ((e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking)) == cudaSuccess &&
+        (e = cudaStreamCreateWithFlags(&alt, cudaStreamNonBlocking)) != cudaSuccess) {
+      cudaStreamDestroy(side);
+    }
     if (e != cudaSuccess) {
       release();
       return cuda_fail(e, "cudaStreamCreate(side)");
     }
     const int32_t* row_of = train ? kperm : nullptr;
     const int bands = (int)band_rows.size() - 1;
+    std::vector<cudaEvent_t> evs(bands + 3, nullptr);
+    for (auto& ev : evs)
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) {
+      cudaEventRecord(evs[bands], st);  // packs, ordering and tiles are ready
+      cudaStreamWaitEvent(alt, evs[bands], 0);
+    }
     for (int b = 0; b < bands && e == cudaSuccess; ++b) {
+      cudaStream_t sb = (b & 1) ? alt : st;
       const int64_t nt = band_tiles[b + 1] - band_tiles[b];
       if (nt > 0) {
         O1Args o{static_cast<const double2*>(bra), static_cast<const double2*>(ket), a.bra_chi,
                  a.n_bras, a.n_kets, npb, nbk, m, a.kind,
                  a.out_mode, dtiles + band_tiles[b], nt, static_cast<double*>(ordered), a.n_kets,
                  bperm, kperm, static_cast<const uint8_t*>(narrow)};
-        overlap_o1_kernel<<<(int)std::min<int64_t>(nt, sms), kWarpsO1 * 32, smem, st>>>(o);
+        overlap_o1_kernel<<<(int)std::min<int64_t>(nt, sms), kWarpsO1 * 32, smem, sb>>>(o);
       }
-      // rows of this band are final once its tiles ran (mirrored entries of
-      // train only ever land in later rows): hand the band to the side stream
-      cudaEvent_t ev;
-      if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) break;
-      cudaEventRecord(ev, st);
-      cudaStreamWaitEvent(side, ev, 0);
-      cudaEventDestroy(ev);
+      cudaEventRecord(evs[b], sb);
+      cudaStreamWaitEvent(side, evs[b], 0);
+      if (b > 0) cudaStreamWaitEvent(side, evs[b - 1], 0);
       const int64_t r0 = band_rows[b], r1 = band_rows[b + 1];
       if (r1 > r0)
         rows_to_host_kernel<<<(int)std::min<int64_t>(r1 - r0, 296), 256, 0, side>>>(
@@ -761,16 +773,24 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
             static_cast<const int32_t*>(kinv), train, a.host_out, a.ld);
       e = cudaGetLastError();
     }
-    // join: the main stream (and the buffer frees below) wait for the last band
-    cudaEvent_t done;
-    if (cudaEventCreateWithFlags(&done, cudaEventDisableTiming) == cudaSuccess) {
-      cudaEventRecord(done, side);
-      cudaStreamWaitEvent(st, done, 0);
-      cudaEventDestroy(done);
+    // join: the main stream (and the buffer frees below) wait for both
+    if (evs[bands + 2]) {
+      cudaEventRecord(evs[bands + 1], alt);
+      cudaStreamWaitEvent(st, evs[bands + 1], 0);
+      cudaEventRecord(evs[bands + 2], side);
+      cudaStreamWaitEvent(st, evs[bands + 2], 0);
     } else {
+      cudaStreamSynchronize(alt);
       cudaStreamSynchronize(side);
     }
+    for (auto ev : evs)
+      if (ev) cudaEventDestroy(ev);
+    cudaStreamDestroy(alt);
     cudaStreamDestroy(side);
+    if (e != cudaSuccess) {
+      release();
+      return cuda_fail(e, "overlap_o1 host streaming");
+    }
   } else if (!tiles.empty()) {
     const size_t smem = o1_smem_bytes(m);
     e = cudaFuncSetAttribute(overlap_o1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
