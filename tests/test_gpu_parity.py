@@ -481,8 +481,10 @@ def test_c_abi_end_to_end_pinned_output_streams_bitwise(native):
                                               C.POINTER(C.c_double)), None, None))
         return out
 
-    for kind, bras, kets in ((N.KIND_TRAIN, X, None), (N.KIND_TEST, Xt, X)):
-        shape = (bras.shape[0], X.shape[0])
+    cases = [(N.KIND_TRAIN, X, None), (N.KIND_TEST, Xt, X), (N.KIND_TRAIN, X[:1].copy(), None),
+             (N.KIND_TRAIN, X[:5].copy(), None), (N.KIND_TEST, Xt[:3].copy(), X[:7].copy())]
+    for kind, bras, kets in cases:
+        shape = (bras.shape[0], bras.shape[0] if kets is None else kets.shape[0])
         ref = call(kind, bras, kets, np.zeros(shape))
         pinned = torch.full(shape, -7.0, dtype=torch.float64).pin_memory()
         got = call(kind, bras, kets, pinned).numpy()
