@@ -8,17 +8,19 @@ Workload (BASELINE.json configs[3] / SURVEY.md 8(d) row 4): m=165 qubits,
 interaction distance d=1, 2 layers, gamma=0.1, per-gate budget 1e-24,
 N=6400 synthetic rows uniform in [0, 2] (seed 0).  One step = encode every
 row, simulate every MPS, fill the whole train kernel (20,476,800 computed
-entries; diagonal and mirror are free) — on N GPUs the rows are sharded,
-the MPS all-gathered once over NCCL and the tiles split block-cyclically
-(total work fixed: strong scaling).
+entries; diagonal and mirror are free).  On N GPUs the rows are sharded, the
+MPS all-gathered once over NCCL without the layout padding, every rank
+computes the K rows of the bra bands it owns (band b -> rank b % N) and rank
+0 gathers and assembles them (total work fixed: strong scaling).
 
 `value` is entries/s with the feature rows already in HBM; `e2e` is the same
-metric through the C ABI (mpskq_gram_host: pinned host rows in, pinned host K
-out, copies inside the timed region) at N=1 and through the public
-run_distributed API at N>1.  The reference arm (--impl reference) times the
-CPU oracle (a numpy restatement of the reference that is bitwise identical
-to it, oracle/mps_oracle.py) on every host core over a bounded sample and
-projects the same metric.
+metric through the public API run_distributed (host rows in, host K out, every
+copy inside the timed region; `e2e_c_abi` is the C ABI mpskq_gram_host under
+it).  `test_kernel` times the headline TEST kernel (1600 test rows x 6400
+train states) with its own roofline.  The reference arm (--impl reference)
+times the CPU oracle (a numpy restatement of the reference that is bitwise
+identical to it, oracle/mps_oracle.py) on every host core over a bounded
+sample and projects the same metric.
 """
 
 from __future__ import annotations
@@ -197,6 +199,23 @@ def fp64_peak_tflops(lib, torch) -> float:
 
 
 # ------------------------------------------------------------------ GPU arm
+def test_flops(chi_b: np.ndarray, chi_k: np.ndarray) -> float:
+    """sum over ALL (bra i, ket j) of F(i,j) (test kind, kernel.py:176-181)."""
+    cb, ck = chi_b.astype(np.float64), chi_k.astype(np.float64)
+    total = 0.0
+    for s in range(cb.shape[1] - 1):
+        # F = 16 chi^k_s chi^b_{s+1} chi^b_s + 16 chi^k_s chi^k_{s+1} chi^b_{s+1}
+        total += 16.0 * (float((cb[:, s + 1] * cb[:, s]).sum()) * float(ck[:, s].sum())
+                         + float(cb[:, s + 1].sum()) * float((ck[:, s] * ck[:, s + 1]).sum()))
+    return total
+
+
+def config_dict(n: int) -> dict:
+    """The workload keys both arms report (identical key sets)."""
+    return {"workload": WORKLOAD, "m": M, "d": D, "layers": R, "gamma": GAMMA, "budget": BUDGET, "N": n,
+            "computed_entries": n * (n - 1) // 2}
+
+
 def gpu_main(args) -> None:
     import torch
     import torch.distributed as dist
@@ -220,12 +239,15 @@ def gpu_main(args) -> None:
         if share:
             dist.init_process_group("gloo")
         else:
+            # communicator setup (ranks, NVLS / channels) in the log for the scaling run
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2411_09336_b200 as P
     from paper_2411_09336_b200 import _native as N
     from paper_2411_09336_b200.ansatz import feature_map_topology
-    from paper_2411_09336_b200.distributed import _all_reduce_max, _reduce_sum_to0, allgather_rows, shard
-    from paper_2411_09336_b200.kernel import encode_device, simulate_rows
+    from paper_2411_09336_b200.distributed import _all_reduce_max, exact_allgather, gather_rows_to0, shard
+    from paper_2411_09336_b200.kernel import simulate_rows
     from paper_2411_09336_b200.mps import batch_layout, compile_program
 
     lib = N.lib()
@@ -253,24 +275,21 @@ def gpu_main(args) -> None:
     peak = torch.empty(nloc, dtype=torch.int32, device=dev)
     status = torch.zeros(nloc, dtype=torch.int32, device=dev)
     counts = [shard(n, world, r)[1] - shard(n, world, r)[0] for r in range(world)]
-    mx = max(counts)
-    nccl = world > 1 and dist.get_backend() == "nccl"
-    if nccl:
-        pad_sites = torch.zeros((mx, 2 * stride), dtype=torch.float64, device=dev)
-        pad_chi = torch.ones((mx, M + 1), dtype=torch.int32, device=dev)
-        g_sites = torch.empty((world * mx, 2 * stride), dtype=torch.float64, device=dev)
-        g_chi = torch.empty((world * mx, M + 1), dtype=torch.int32, device=dev)
-    if world > 1:
-        sites_all = torch.empty((n, 2 * stride), dtype=torch.float64, device=dev)
-        chi_all = torch.empty((n, M + 1), dtype=torch.int32, device=dev)
-    else:
-        sites_all, chi_all = sites_loc, chi_loc
     K = torch.empty((n, n), dtype=torch.float64, device=dev)
+    if world > 1:
+        n_own = N.C.c_int64(0)
+        N.check(lib.mpskq_owned_rows(cap, n, rank, world, N.C.byref(n_own)))
+        rows = torch.empty((n_own.value, n), dtype=torch.float64, device=dev)
+        ids = torch.empty(n_own.value, dtype=torch.int32, device=dev)
+        pos = torch.empty(n, dtype=torch.int32, device=dev)
+    comm = {"allgather_bytes_received": 0, "gather_bytes_to_rank0": 0}
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
-    # ours per step: encode, simulate, ket key, chi=4 clustering, block bounds, inverse
-    # order, pack bras, pack kets, overlap, un-permute, diagonal (rank 0); the ket
-    # key sort is CUB's radix sort (library, not counted)
-    launches_per_step = 10 + (1 if rank == 0 else 0)
+    # ours per step: encode, simulate, ket key, chi=4 clustering, block bounds,
+    # inverse order, pack bras, pack kets, overlap, un-permute / owned rows,
+    # diagonal (N=1); N>1 adds exact pack + unpack and, on rank 0, scatter +
+    # mirror.  The ket key sort is CUB's radix sort (library, not counted).
+    launches_per_step = (11 if world == 1 else 12 + (2 if rank == 0 else 0))
+    state = {"sites_all": sites_loc, "chi_all": chi_loc}
 
     def step(e):
         e[0].record()
@@ -280,30 +299,26 @@ def gpu_main(args) -> None:
                                    prog.n_params, nloc, BUDGET, 0, off_d.data_ptr(), stride, sites_loc.data_ptr(),
                                    chi_loc.data_ptr(), disc.data_ptr(), peak.data_ptr(), status.data_ptr(), None, sp))
         e[1].record()
-        if nccl:  # the one exchange: all-gather of the packed MPS + bond dims
-            pad_sites[:nloc].copy_(sites_loc)
-            pad_chi[:nloc].copy_(chi_loc)
-            dist.all_gather_into_tensor(g_sites, pad_sites)
-            dist.all_gather_into_tensor(g_chi, pad_chi)
-            o = 0
-            for r, c in enumerate(counts):
-                sites_all[o : o + c].copy_(g_sites[r * mx : r * mx + c])
-                chi_all[o : o + c].copy_(g_chi[r * mx : r * mx + c])
-                o += c
-        elif world > 1:
-            sites_all.copy_(allgather_rows(sites_loc, counts))
-            chi_all.copy_(allgather_rows(chi_loc, counts))
-        if world > 1:
-            K.zero_()
+        if world > 1:  # the one exchange: exact (unpadded) all-gather of the MPS
+            sa, ca, recv = exact_allgather(sites_loc, chi_loc, counts, M, stride, off_d)
+            state["sites_all"], state["chi_all"] = sa, ca
+            comm["allgather_bytes_received"] = recv
         e[2].record()
-        N.check(lib.mpskq_overlap(N.KIND_TRAIN, N.OUT_KERNEL, M, cap, off_d.data_ptr(), stride, sites_all.data_ptr(),
-                                  chi_all.data_ptr(), n, sites_all.data_ptr(), chi_all.data_ptr(), n, rank, world,
-                                  K.data_ptr(), n, sp))
-        e[3].record()
-        if nccl:
-            dist.reduce(K, dst=0, op=dist.ReduceOp.SUM)
-        elif world > 1:
-            K.copy_(_reduce_sum_to0(K))
+        sa, ca = state["sites_all"], state["chi_all"]
+        if world == 1:
+            N.check(lib.mpskq_overlap(N.KIND_TRAIN, N.OUT_KERNEL, M, cap, off_d.data_ptr(), stride, sa.data_ptr(),
+                                      ca.data_ptr(), n, sa.data_ptr(), ca.data_ptr(), n, 0, 1, K.data_ptr(), n, sp))
+            e[3].record()
+        else:
+            N.check(lib.mpskq_overlap_owned_rows(N.KIND_TRAIN, M, cap, off_d.data_ptr(), stride, sa.data_ptr(),
+                                                 ca.data_ptr(), n, sa.data_ptr(), ca.data_ptr(), n, rank, world,
+                                                 rows.data_ptr(), ids.data_ptr(), pos.data_ptr(), sp))
+            e[3].record()
+            all_rows, all_ids = gather_rows_to0(rows, ids)
+            if rank == 0:
+                comm["gather_bytes_to_rank0"] = int(all_rows.numel() * 8 - rows.numel() * 8)
+                N.check(lib.mpskq_assemble_rows(N.KIND_TRAIN, n, n, all_rows.data_ptr(), all_ids.data_ptr(),
+                                                all_ids.shape[0], pos.data_ptr(), K.data_ptr(), n, sp))
         e[4].record()
 
     for _ in range(args.warmup):
@@ -335,7 +350,8 @@ def gpu_main(args) -> None:
         ms, sim_ms, comm_ms, ov_ms, red_ms = _all_reduce_max(t).tolist()
 
     # parity spot check of this very run against the CPU oracle (rows 0..5)
-    spot = None
+    spot = chi_ok = None
+    chi_all = state["chi_all"]
     if rank == 0:
         from oracle import mps_oracle as O
 
@@ -343,9 +359,47 @@ def gpu_main(args) -> None:
         Ko = O.gram([s.sites for s in sub], [s.sites for s in sub], "train")
         spot = float(np.abs(K[:6, :6].cpu().numpy() - Ko).max())
         chi_ok = bool(np.array_equal(chi_all[:6].cpu().numpy(), np.array([s.bond_dims() for s in sub])))
+    K_dev_np = K.cpu().numpy() if rank == 0 else None
 
-    # e2e through the host-buffer entry points
-    e2e = None
+    # e2e through the public API: run_distributed (kernel.py:443-512) with
+    # host rows in and the host K out (N=1: one native call that streams K
+    # into page-locked memory under the overlap; N>1: sharded + gathered)
+    sched = P.make_schedule(n, n, world, "round_robin", "train")
+    for _ in range(max(1, args.warmup)):
+        g = P.run_distributed(X, X, cfg, sched, budget=BUDGET)
+    del g
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    a.record()
+    k_equal = None
+    for k in range(args.steps):
+        g = P.run_distributed(X, X, cfg, sched, budget=BUDGET)
+        if k == args.steps - 1 and rank == 0:
+            last = g
+        del g
+    b.record()
+    b.synchronize()
+    if world > 1:
+        dist.barrier()
+    e2e_ms = a.elapsed_time(b) / args.steps
+    wall_ms = 1e3 * (time.perf_counter() - w0) / args.steps
+    if world > 1:
+        e2e_ms, wall_ms = _all_reduce_max(torch.tensor([e2e_ms, wall_ms], dtype=torch.float64, device=dev)).tolist()
+    if rank == 0:
+        k_equal = bool(np.array_equal(last.entries, K_dev_np))
+        del last
+    e2e = {"value": n * (n - 1) / 2 / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": X.nbytes,
+           "d2h_bytes_per_step": n * n * 8, "ms_per_step": e2e_ms, "host_wall_ms_per_step": wall_ms,
+           "path": "public API run_distributed(X, X, cfg, make_schedule(N, N, n_gpus, 'round_robin', 'train')): "
+                   "host rows -> host K (N=1: mpskq_gram_host streams K row bands into page-locked memory "
+                   "under the overlap)",
+           "k_bitwise_equal_device_path": k_equal}
+
+    # the C ABI itself (what a non-Python binding calls), N=1
+    e2e_c = None
     if world == 1:
         import ctypes as C
 
@@ -361,36 +415,75 @@ def gpu_main(args) -> None:
 
         for _ in range(max(1, args.warmup)):
             host_call()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        w0 = time.perf_counter()
         a.record()
         for _ in range(args.steps):
             host_call()
         b.record()
         b.synchronize()
-        e2e_ms = a.elapsed_time(b) / args.steps
-        wall_ms = 1e3 * (time.perf_counter() - w0) / args.steps
-        e2e = {"value": n * (n - 1) / 2 / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": X.nbytes,
-               "d2h_bytes_per_step": n * n * 8, "ms_per_step": e2e_ms, "host_wall_ms_per_step": wall_ms,
-               "path": "C ABI mpskq_gram_host (pinned host rows -> pinned host K, row bands streamed "
-                       "to host under the overlap)",
-               "k_bitwise_equal_device_path": bool(torch.equal(Kp, K.cpu()))}
-    else:
-        sched = P.make_schedule(n, n, world, "round_robin", "train")
-        for _ in range(max(1, args.warmup)):
-            P.run_distributed(X, X, cfg, sched, budget=BUDGET)
-        dist.barrier()
+        ms_c = a.elapsed_time(b) / args.steps
+        e2e_c = {"value": n * (n - 1) / 2 / (ms_c / 1e3), "ms_per_step": ms_c,
+                 "path": "C ABI mpskq_gram_host (pinned host rows -> pinned host K)"}
+        del Kp
+
+    # the headline TEST kernel (BASELINE configs[3]: M=1600 test rows x N
+    # train states, kernel.py:176-181): simulate the test rows and fill M x N
+    # against the resident train states (the inference use)
+    test_line = None
+    if world == 1 and args.test_rows > 0:
+        mt = args.test_rows
+        Xt = feature_rows(mt, seed=1)
+        Xt_d = torch.from_numpy(Xt).to(dev)
+        coef_t = torch.empty((mt, prog.n_params, 2), dtype=torch.float64, device=dev)
+        sites_t = torch.empty((mt, 2 * stride), dtype=torch.float64, device=dev)
+        chi_t = torch.empty((mt, M + 1), dtype=torch.int32, device=dev)
+        disc_t = torch.empty(mt, dtype=torch.float64, device=dev)
+        peak_t = torch.empty(mt, dtype=torch.int32, device=dev)
+        status_t = torch.zeros(mt, dtype=torch.int32, device=dev)
+        Kt = torch.empty((mt, n), dtype=torch.float64, device=dev)
+        evt = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+
+        def tstep(e):
+            e[0].record()
+            N.check(lib.mpskq_feature_map_coefficients_device(Xt_d.data_ptr(), mt, M, R, D, GAMMA,
+                                                              coef_t.data_ptr(), bad.data_ptr(), sp))
+            N.check(lib.mpskq_simulate(M, cap, ops.data_ptr(), prog.ops.shape[0], prog.n_gates, coef_t.data_ptr(),
+                                       prog.n_params, mt, BUDGET, 0, off_d.data_ptr(), stride, sites_t.data_ptr(),
+                                       chi_t.data_ptr(), disc_t.data_ptr(), peak_t.data_ptr(), status_t.data_ptr(),
+                                       None, sp))
+            e[1].record()
+            N.check(lib.mpskq_overlap(N.KIND_TEST, N.OUT_KERNEL, M, cap, off_d.data_ptr(), stride,
+                                      sites_t.data_ptr(), chi_t.data_ptr(), mt, sites_loc.data_ptr(),
+                                      chi_loc.data_ptr(), n, 0, 1, Kt.data_ptr(), n, sp))
+            e[2].record()
+
+        for _ in range(args.warmup):
+            tstep(evt[0])
         torch.cuda.synchronize()
-        w0 = time.perf_counter()
-        for _ in range(args.steps):
-            P.run_distributed(X, X, cfg, sched, budget=BUDGET)
-        torch.cuda.synchronize()
-        dist.barrier()
-        t = torch.tensor([(time.perf_counter() - w0) / args.steps], dtype=torch.float64, device=dev)
-        e2e_ms = 1e3 * _all_reduce_max(t).item()
-        e2e = {"value": n * (n - 1) / 2 / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": X.nbytes,
-               "d2h_bytes_per_step": n * n * 8, "ms_per_step": e2e_ms,
-               "path": "public API run_distributed (host rows -> host K on rank 0), max over ranks"}
+        if int(status_t.max().item()) != 0:
+            raise RuntimeError("test-row simulation reported a bad state")
+        a.record()
+        for k in range(args.steps):
+            tstep(evt[k])
+        b.record()
+        b.synchronize()
+        t_ms = a.elapsed_time(b) / args.steps
+        t_ov = float(np.mean([e[1].elapsed_time(e[2]) for e in evt]))
+        t_sim = float(np.mean([e[0].elapsed_time(e[1]) for e in evt]))
+        tfl = test_flops(chi_t.cpu().numpy(), chi_loc.cpu().numpy())
+        from oracle import mps_oracle as O
+
+        sub_t = [O.simulate_row(x, M, R, D, GAMMA, BUDGET) for x in Xt[:3]]
+        sub = [O.simulate_row(x, M, R, D, GAMMA, BUDGET) for x in X[:4]]
+        Kto = O.gram([s.sites for s in sub_t], [s.sites for s in sub], "test")
+        test_line = {
+            "workload": f"headline test kernel: {mt} test rows (seed 1) x {n} train states (BASELINE configs[3])",
+            "entries": mt * n, "value": mt * n / (t_ms / 1e3), "unit": UNIT, "ms_per_step": t_ms,
+            "phases_ms": {"simulate_test_rows": t_sim, "overlap": t_ov},
+            "roofline": None,  # filled below with the same peak
+            "algorithmic_flops_per_launch": tfl,
+            "parity_spot_check": {"max_abs_err_vs_oracle_3x4": float(np.abs(Kt[:3, :4].cpu().numpy() - Kto).max())},
+        }
+        del Kt, sites_t
 
     if rank != 0:
         if world > 1:
@@ -407,6 +500,11 @@ def gpu_main(args) -> None:
             traffic = json.loads(tfile.read_text()).get("overlap_o1_bytes_per_launch")
         except (ValueError, OSError):
             traffic = None
+    if test_line is not None:
+        ach_t = test_line["algorithmic_flops_per_launch"] / (test_line["phases_ms"]["overlap"] / 1e3) / 1e12
+        test_line["roofline"] = {"bound": "fp64", "achieved": ach_t, "peak": peak_tf, "unit": "TFLOP/s",
+                                 "frac": ach_t / peak_tf if peak_tf else None,
+                                 "kernel": "overlap_o1_kernel, test kind (whole mpskq_overlap call)"}
     entries = n * (n - 1) / 2
     line = {
         "metric": METRIC,
@@ -421,17 +519,17 @@ def gpu_main(args) -> None:
         "vs_baseline": entries / (ms / 1e3) / PUBLISHED_ENTRIES_PER_S,
         "dtype": "c128",
         "data": "synthetic: rows uniform [0,2] (seed 0); no trained weights exist for this path",
-        "config": {
-            "workload": WORKLOAD,
-            "m": M, "d": D, "layers": R, "gamma": GAMMA, "budget": BUDGET, "N": n,
-            "computed_entries": int(entries),
-            "parallelism": f"rows sharded x{world}, MPS all-gathered once, tiles block-cyclic",
+        "config": config_dict(n),
+        "layout": {
+            "parallelism": (f"rows sharded x{world}, MPS all-gathered once (exact, unpadded), K rows owned "
+                            f"band-cyclically and gathered to rank 0" if world > 1 else "one GPU"),
             "l2": "working set (540 MB padded MPS + 328 MB K) larger than L2; no flush needed",
             "chi_cap": cap,
         },
         "train_wall_s": ms / 1e3,
         "mps_states_per_s": n / (sim_ms / 1e3),
-        "phases_ms": {"simulate": sim_ms, "all_gather": comm_ms, "overlap": ov_ms, "reduce": red_ms},
+        "phases_ms": {"simulate": sim_ms, "all_gather": comm_ms, "overlap": ov_ms, "gather_assemble": red_ms},
+        "communication_bytes_per_step": comm if world > 1 else None,
         "roofline": {
             "bound": "fp64",
             "kernel": "overlap_o1_kernel (timed as the whole mpskq_overlap call: ket ordering + 2 packs + overlap + diagonal)",
@@ -446,6 +544,8 @@ def gpu_main(args) -> None:
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
         "e2e": e2e,
+        "e2e_c_abi": e2e_c,
+        "test_kernel": test_line,
         "gpu_launches": launches_per_step * args.steps,
         "parity_spot_check": {"max_abs_err_vs_oracle_6x6": spot, "bond_dims_equal": chi_ok},
     }
@@ -486,8 +586,7 @@ def reference_main(args) -> None:
         "vs_baseline": v / PUBLISHED_ENTRIES_PER_S,
         "dtype": "c128",
         "data": "synthetic: rows uniform [0,2] (seed 0)",
-        "config": {"workload": WORKLOAD, "m": M, "d": D, "layers": R, "gamma": GAMMA, "budget": BUDGET, "N": n,
-                   "computed_entries": n * (n - 1) // 2},
+        "config": config_dict(n),
         "train_wall_s": float(np.median(walls)),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": s["cores"], "kind": "port", "sample": s["sample"]},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -504,6 +603,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--rows", type=int, default=6400, help="N feature rows (train kernel N x N)")
+    ap.add_argument("--test-rows", type=int, default=1600, help="M test rows of the headline test kernel (0: skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=8.0)

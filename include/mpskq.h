@@ -44,6 +44,7 @@ extern "C" {
 #define MPSKQ_STATE_OK 0
 #define MPSKQ_STATE_CAPACITY 1
 #define MPSKQ_STATE_NONFINITE 2
+#define MPSKQ_STATE_NOCONV 3 /* Jacobi SVD without a quiet cycle in 40 sweeps (zgesdd's LinAlgError) */
 
 /* gate kinds (ansatz.py:15 GATE_KINDS order) */
 #define MPSKQ_GATE_H 0
@@ -58,6 +59,10 @@ extern "C" {
 #define MPSKQ_OP_SWAP 4 /* apply_two_qubit with SWAP       mps.py:163-205, ansatz.py:77-79 */
 #define MPSKQ_OP_QRL 5  /* one _left_isometrize step       mps.py:105-111 */
 #define MPSKQ_OP_QRR 6  /* one _right_isometrize step      mps.py:114-120 */
+#define MPSKQ_OP_U1 7   /* apply_one_qubit with an arbitrary 2x2 matrix: 4 complex coefficients
+                           (row-major) from param_slot on              mps.py:147-160 */
+#define MPSKQ_OP_U2 8   /* apply_two_qubit with an arbitrary 4x4 matrix on |q, q+1>: 16 complex
+                           coefficients (row-major) from param_slot on mps.py:163-205 */
 #define MPSKQ_ABSORB_LEFT 1
 
 /* kinds of Gram matrix (kernel.py:31 KINDS) */
@@ -143,6 +148,42 @@ int mpskq_simulate(int m, int chi_cap, const int32_t* ops_dev, int64_t n_ops, in
                    int32_t* peak_chi_dev, int32_t* status_dev, int64_t* entry_log_dev,
                    void* stream);
 
+/* General form of mpskq_simulate.  from_input != 0 continues the states
+ * already held in sites/chi/discard/peak_chi (same layout) instead of
+ * starting from |0..0>: apply_gate / canonicalize / run_circuit on a given
+ * MpsState (mps.py:123-247) are op programs replayed this way (QRL/QRR moves
+ * from the state's ortho_center, U1/U2 ops for arbitrary matrices whose
+ * coefficients sit in coef_dev).  phase_cycles_dev (nullable, n_states x 3
+ * int64) receives the device clock cycles each state spent in
+ * {canonicalize, one_qubit, two_qubit} ops (MpsState.timings keys,
+ * mps.py:137, :159, :204).                                                */
+int mpskq_run_program(int m, int chi_cap, const int32_t* ops_dev, int64_t n_ops, int64_t n_gates,
+                      const double* coef_dev, int64_t n_params, int64_t n_states, double budget,
+                      int chi_max, const int64_t* site_off_dev, int64_t state_stride,
+                      int from_input, double* sites_dev, int32_t* chi_dev, double* discard_dev,
+                      int32_t* peak_chi_dev, int32_t* status_dev, int64_t* entry_log_dev,
+                      int64_t* phase_cycles_dev, void* stream);
+
+/* Move n states between chi-capacity layouts (mpskq_batch_layout): state i
+ * of src (bond dims chi_dev row i) becomes row dst_rows_dev[i] of dst
+ * (identity when NULL).  Used by per-state capacity escalation: only the
+ * states that overflowed a capacity are re-simulated at a larger one.     */
+int mpskq_relayout(int m, int64_t n, const double* src_sites_dev, const int64_t* src_off_dev,
+                   int64_t src_stride, const int32_t* chi_dev, double* dst_sites_dev,
+                   const int64_t* dst_off_dev, int64_t dst_stride, const int32_t* dst_rows_dev,
+                   void* stream);
+
+/* Exact (unpadded) packing of n states for the multi-GPU exchange: state i's
+ * site tensors back to back ((chi_l, 2, chi_r) row-major, the MPS1 payload
+ * order, mps.py:294-314) from complex offset state_off_dev[i]; the caller
+ * computes state_off as the prefix sum of sum_s 2 chi_s chi_{s+1}.  Unpack
+ * is the inverse into a batch layout.                                     */
+int mpskq_pack_exact(int m, int64_t n, const double* sites_dev, const int64_t* site_off_dev, int64_t state_stride,
+                     const int32_t* chi_dev, const int64_t* state_off_dev, double* packed_dev, void* stream);
+int mpskq_unpack_exact(int m, int64_t n, const double* packed_dev, const int64_t* state_off_dev,
+                       const int32_t* chi_dev, double* sites_dev, const int64_t* site_off_dev, int64_t state_stride,
+                       void* stream);
+
 /* ---------------------------------------------------------------- truncated SVD
  * svd_truncated (tensor.py:87-123) on a batch of rows x cols complex
  * matrices (row-major, contiguous).  Outputs per matrix: U (rows x kmin),
@@ -194,6 +235,40 @@ int mpskq_overlap_tiles(int kind, int chi_cap, int64_t n_bras, int64_t n_kets, i
 int mpskq_gram_host(int kind, int m, int r, int d, double gamma, double budget, int chi_max,
                     int chi_cap, const double* X_bras, int64_t n_bras, const double* X_kets,
                     int64_t n_kets, double* K_out, void* stream, double* seconds);
+
+/* Multi-GPU row ownership (replaces the dense N x N sum-reduce): rank r
+ * computes the K rows of the bra bands it owns (band b -> rank b % world;
+ * bands of 8 ordered rows on the chi <= 4 path, single rows otherwise) and
+ * writes them compactly, caller column order: rows_out[k * n_kets + j] is
+ * caller row row_ids[k] (-1 = padding).  mpskq_owned_rows gives the row
+ * count to allocate.  Train rows hold the entries this rank computed; the
+ * gatherer's mpskq_assemble_rows scatters every rank's rows into K and
+ * mirrors the rest with ket_pos (the ordered position of every state,
+ * written by any rank's call; identity off the chi <= 4 path) plus the unit
+ * diagonal — compute_gram's result (kernel.py:165-181).                   */
+int mpskq_owned_rows(int chi_cap, int64_t n_bras, int rank, int world, int64_t* n_owned);
+int mpskq_overlap_owned_rows(int kind, int m, int chi_cap, const int64_t* site_off_dev, int64_t state_stride,
+                             const double* bra_sites_dev, const int32_t* bra_chi_dev, int64_t n_bras,
+                             const double* ket_sites_dev, const int32_t* ket_chi_dev, int64_t n_kets, int rank,
+                             int world, double* rows_out_dev, int32_t* row_ids_dev, int32_t* ket_pos_dev,
+                             void* stream);
+int mpskq_assemble_rows(int kind, int64_t n_bras, int64_t n_kets, const double* rows_dev,
+                        const int32_t* row_ids_dev, int64_t n_rows, const int32_t* ket_pos_dev, double* K_dev,
+                        int64_t ld, void* stream);
+
+/* compute_gram (kernel.py:147-185) of device-resident states into HOST
+ * memory K_out (n_bras x n_kets, row-major): a page-locked K_out on the
+ * chi <= 4 path receives row bands while the overlap still runs (as in
+ * mpskq_gram_host); otherwise device K plus one copy.  Train writes the
+ * unit diagonal and the mirror.  Returns after K_out is complete.         */
+int mpskq_overlap_host(int kind, int m, int chi_cap, const int64_t* site_off_dev, int64_t state_stride,
+                       const double* bra_sites_dev, const int32_t* bra_chi_dev, int64_t n_bras,
+                       const double* ket_sites_dev, const int32_t* ket_chi_dev, int64_t n_kets,
+                       double* K_out, void* stream);
+
+/* SM clock of the current device in kHz (cudaDevAttrClockRate; 0 without a
+ * device): converts mpskq_run_program's phase cycles into seconds.        */
+int mpskq_sm_clock_khz(void);
 
 /* FP64 FMA throughput probe (roofline denominator): n_blocks x 256 threads,
  * each running `iters` x 16 independent DFMA.  Writes a checksum to out_dev. */

@@ -39,9 +39,14 @@ from .mps import (
     MpsBatch,
     MpsState,
     SimStats,
+    apply_gate,
+    apply_one_qubit,
+    apply_two_qubit,
+    canonicalize,
     deserialize_state,
     init_state,
     inner_product,
+    run_circuit,
     serialize_state,
     simulate_circuit,
     stats,

@@ -21,7 +21,9 @@ ERR_CUDA = -2
 ERR_CAPACITY = -3
 ERR_NUMERIC = -4
 ERR_NOMEM = -5
-STATE_OK, STATE_CAPACITY, STATE_NONFINITE = 0, 1, 2
+STATE_OK, STATE_CAPACITY, STATE_NONFINITE, STATE_NOCONV = 0, 1, 2, 3
+OP_H, OP_RZ, OP_RXX, OP_SWAP, OP_QRL, OP_QRR, OP_U1, OP_U2 = 1, 2, 3, 4, 5, 6, 7, 8
+ABSORB_LEFT = 1
 
 GATE_H, GATE_RZ, GATE_RXX, GATE_SWAP = 0, 1, 2, 3
 KIND_TRAIN, KIND_TEST = 0, 1
@@ -60,6 +62,15 @@ _SIGNATURES = {
         [C.c_int, C.c_int, _vp, C.c_int64, C.c_int64, _vp, C.c_int64, C.c_int64, C.c_double,
          C.c_int, _vp, C.c_int64, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     ),
+    "mpskq_run_program": (
+        C.c_int,
+        [C.c_int, C.c_int, _vp, C.c_int64, C.c_int64, _vp, C.c_int64, C.c_int64, C.c_double,
+         C.c_int, _vp, C.c_int64, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    ),
+    "mpskq_relayout": (
+        C.c_int,
+        [C.c_int, C.c_int64, _vp, _vp, C.c_int64, _vp, _vp, _vp, C.c_int64, _vp, _vp],
+    ),
     "mpskq_svd_truncated_batched": (
         C.c_int,
         [C.c_int, C.c_int, C.c_int64, _vp, C.c_double, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
@@ -68,6 +79,22 @@ _SIGNATURES = {
         C.c_int,
         [C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.c_int64, _vp, _vp, C.c_int64, _vp, _vp,
          C.c_int64, C.c_int, C.c_int, _vp, C.c_int64, _vp],
+    ),
+    "mpskq_pack_exact": (C.c_int, [C.c_int, C.c_int64, _vp, _vp, C.c_int64, _vp, _vp, _vp, _vp]),
+    "mpskq_unpack_exact": (C.c_int, [C.c_int, C.c_int64, _vp, _vp, _vp, _vp, _vp, C.c_int64, _vp]),
+    "mpskq_owned_rows": (C.c_int, [C.c_int, C.c_int64, C.c_int, C.c_int, _i64p]),
+    "mpskq_overlap_owned_rows": (
+        C.c_int,
+        [C.c_int, C.c_int, C.c_int, _vp, C.c_int64, _vp, _vp, C.c_int64, _vp, _vp, C.c_int64, C.c_int, C.c_int,
+         _vp, _vp, _vp, _vp],
+    ),
+    "mpskq_assemble_rows": (
+        C.c_int,
+        [C.c_int, C.c_int64, C.c_int64, _vp, _vp, C.c_int64, _vp, _vp, C.c_int64, _vp],
+    ),
+    "mpskq_overlap_host": (
+        C.c_int,
+        [C.c_int, C.c_int, C.c_int, _vp, C.c_int64, _vp, _vp, C.c_int64, _vp, _vp, C.c_int64, _vp, _vp],
     ),
     "mpskq_overlap_tiles": (
         C.c_int,
@@ -78,6 +105,7 @@ _SIGNATURES = {
         [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, _f64p,
          C.c_int64, _f64p, C.c_int64, _f64p, _vp, _f64p],
     ),
+    "mpskq_sm_clock_khz": (C.c_int, []),
     "mpskq_fp64_probe": (C.c_int, [C.c_int, C.c_int64, _vp, _vp]),
 }
 

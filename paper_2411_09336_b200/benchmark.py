@@ -2,13 +2,13 @@
 reference's ``cli.cmd_benchmark`` (cli.py:240-294) without its dataset/CLI
 plumbing (out of scope).
 
-The reference times each sample's ``simulate_circuit`` and each pairwise
-``inner_product`` on the CPU and records the peak bond dimension per sample
-and the state memory after every gate (``memory_log``, mps.py:245-246).  On
-the GPU all samples are simulated in one batched launch and all pairs in one
-overlap launch, so the per-sample / per-pair seconds reported here are the
-batch device times divided by the counts (CUDA events), and the memory
-series come from the simulator's per-gate entry log.
+Like the reference, every sample's simulation and every pairwise inner
+product is timed on its own: one single-state simulation launch per sample
+and one single-pair overlap launch per pair, each bracketed by CUDA events
+on the launching stream (device latency of one unit, not a batch time
+divided by the count).  The peak bond dimension per sample and the state
+memory after every gate (``memory_log``, mps.py:245-246) come from the
+simulator's per-gate entry log.
 """
 
 from __future__ import annotations
@@ -33,24 +33,45 @@ def benchmark_rows(X, cfg: FeatureMapConfig, budget: float = DEFAULT_TRUNC_BUDGE
     n = X.shape[0]
     if n < 2:
         raise ValueError("benchmark needs at least 2 samples")
+    # encode_circuit's row checks (ansatz.py:121-124)
+    if not np.all(np.isfinite(X)):
+        raise ValueError("features must be finite")
+    if np.any((X < 0.0) | (X > 2.0)):
+        raise ValueError("features must lie in [0, 2]; rescale the data first")
     prog = compile_program(feature_map_topology(cfg.m, cfg.r, cfg.d))
-    coef, _ = encode_device(torch.from_numpy(np.ascontiguousarray(X)).to("cuda"), cfg)
-    batch = simulate_program(prog, coef, budget, memory_log=True)
-    with Timer() as t_ov:
-        overlap_matrix(batch, batch, "test", amplitude=True)
-    pairs = n * (n - 1) // 2
-    # the test-kind launch evaluates all n^2 pairs; scale to the i<j count
-    ip = t_ov.seconds() / (n * n)
-    sim = batch.seconds / n
-    states = batch.to_states()
-    max_chi = [max(s.peak_chi, s.max_bond()) for s in states]
+    coef, bad = encode_device(torch.from_numpy(np.ascontiguousarray(X)).to("cuda"), cfg)
+    if int(bad.item()) != 0:
+        raise ValueError("features must lie in [0, 2]; rescale the data first")
+    # warm the program / capacity hint so the per-sample launches are steady
+    simulate_program(prog, coef[:1], budget)
+    states, sim_times = [], []
+    for i in range(n):
+        with Timer() as t:
+            b = simulate_program(prog, coef[i : i + 1], budget, memory_log=True)
+        sim_times.append(t.seconds())
+        states.append(b)
+    cap = max(b.chi_cap for b in states)
+    ip_times = []
+    for i in range(n):
+        for j in range(i + 1, n):
+            a, k = states[i], states[j]
+            if a.chi_cap != cap or k.chi_cap != cap:  # one layout per pair launch
+                from .mps import MpsBatch
+
+                a = a if a.chi_cap == cap else MpsBatch.from_states(a.to_states(), cap)
+                k = k if k.chi_cap == cap else MpsBatch.from_states(k.to_states(), cap)
+                states[i], states[j] = a, k
+            with Timer() as t:
+                overlap_matrix(a, k, "test", amplitude=True)
+            ip_times.append(t.seconds())
+    single = [b[0] for b in states]
     return {
         "samples": n,
-        "simulation_seconds": [sim] * n,
-        "inner_product_seconds": [ip] * pairs,
-        "simulation_summary": _summary([sim] * n),
-        "inner_product_summary": _summary([ip] * pairs),
-        "max_chi": max_chi,
-        "memory_bytes_per_gate": [batch.memory_log(i) for i in range(n)],
-        "timing": "batched device time divided by the number of states / pairs (CUDA events)",
+        "simulation_seconds": sim_times,
+        "inner_product_seconds": ip_times,
+        "simulation_summary": _summary(sim_times),
+        "inner_product_summary": _summary(ip_times),
+        "max_chi": [max(s.peak_chi, s.max_bond()) for s in single],
+        "memory_bytes_per_gate": [b.memory_log(0) for b in states],
+        "timing": "per sample / per pair: one launch each, CUDA events on the launching stream",
     }

@@ -50,6 +50,8 @@ struct SimArgs {
   int32_t* status;
   int64_t* entry_log;
   void* scratch;  // set by the launcher (rotation logs of capacities > 32)
+  int from_input = 0;                // continue the states already in sites/chi/discard/peak
+  long long* phase_cycles = nullptr;  // n_states x {canonicalize, one_qubit, two_qubit}
 };
 int launch_simulate(const SimArgs& a, void* stream);
 
@@ -85,8 +87,32 @@ struct OverlapArgs {
   // tiles and a side stream writes each finished row band straight into host
   // memory while the next band computes; `out` is not touched.
   double* host_out = nullptr;
+  // optional (world > 1): row ownership instead of tile ownership.  The rank
+  // computes the rows of the bra bands it owns (band b -> rank b % world;
+  // O1: bands of 8 ordered rows, generic: single rows) and writes them
+  // compactly in caller column order: rows_out[k * n_kets + j], caller row
+  // row_ids_out[k].  Train rows hold only the entries the rank computed
+  // (ordered i < j); mpskq_assemble_rows mirrors the rest on the gatherer.
+  // ket_pos_out (nullable): ordered position of every ket (train mirror).
+  double* rows_out = nullptr;
+  int32_t* row_ids_out = nullptr;
+  int32_t* ket_pos_out = nullptr;
 };
+// rows of n_bras owned by `rank` under row ownership for this capacity
+int64_t owned_row_count(int chi_cap, int64_t n_bras, int rank, int world);
 int launch_overlap(const OverlapArgs& a, void* stream);
+
+// move states between chi-capacity layouts: src row i -> dst row dst_rows[i]
+int launch_relayout(int m, int64_t n, const double* src, const int64_t* src_off, int64_t src_stride,
+                    const int32_t* chi, double* dst, const int64_t* dst_off, int64_t dst_stride,
+                    const int32_t* dst_rows, void* stream);
+
+// dst row dst_idx[i] = src row src_idx[i] (nullable indices = identity)
+int launch_copy_rows(const void* src, void* dst, int64_t row_bytes, int64_t n, const int32_t* src_idx,
+                     const int32_t* dst_idx, void* stream);
+
+int launch_pack_exact(int m, int64_t n, double* sites, const int64_t* site_off, int64_t stride, const int32_t* chi,
+                      const int64_t* state_off, double* packed, int unpack, void* stream);
 
 int launch_encode(const double* X, int64_t n_rows, int m, int r, int d, double gamma, double* coef,
                   int* bad, void* stream);

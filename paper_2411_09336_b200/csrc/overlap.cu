@@ -201,6 +201,22 @@ __global__ void rows_to_host_kernel(const double* __restrict__ ordered, int64_t 
   }
 }
 
+// Row ownership (world > 1): the k-th owned row is ordered row
+// o = (band(k) * world + rank) * rb + k % rb; gather it in caller column
+// order into the compact block and record its caller row id.
+__global__ void owned_rows_kernel(const double* __restrict__ ordered, int64_t n_rows, int64_t nk, int rb,
+                                  int rank, int world, const int32_t* __restrict__ row_of,
+                                  const int32_t* __restrict__ kpos, double* __restrict__ out,
+                                  int32_t* __restrict__ ids, int64_t n_owned) {
+  for (int64_t k = blockIdx.x; k < n_owned; k += gridDim.x) {
+    const int64_t o = ((k / rb) * world + rank) * rb + k % rb;
+    if (o >= n_rows) continue;
+    const double* row = ordered + o * nk;
+    for (int64_t b = threadIdx.x; b < nk; b += blockDim.x) out[k * nk + b] = row[kpos ? kpos[b] : b];
+    if (threadIdx.x == 0) ids[k] = row_of ? row_of[o] : (int32_t)o;
+  }
+}
+
 __device__ __forceinline__ void store_result(int out_mode, double* out, int64_t ld, int64_t i,
                                              int64_t j, double2 ov, bool mirror) {
   if (out_mode == MPSKQ_OUT_KERNEL) {
@@ -598,7 +614,7 @@ inline int64_t super_rows(int rb) { return std::max<int64_t>(1, 384 / rb); }
 // [i_lo, i_hi): row-block range (the host-streaming path enumerates one
 // super-row at a time; the default covers every row block)
 std::vector<int2> make_tiles(bool train, int64_t n_rows, int64_t n_cols, int rb, int cb, int rank,
-                             int world, int64_t i_lo = 0, int64_t i_hi = -1) {
+                             int world, int64_t i_lo = 0, int64_t i_hi = -1, bool by_band = false) {
   std::vector<int2> tiles;
   const int64_t nrb = (n_rows + rb - 1) / rb, ncb = (n_cols + cb - 1) / cb;
   const int64_t sr = super_rows(rb), sc = std::max<int64_t>(1, 384 / cb);
@@ -610,7 +626,8 @@ std::vector<int2> make_tiles(bool train, int64_t n_rows, int64_t n_cols, int rb,
         const int64_t jmax = std::min(n_cols, (J + 1) * cb) - 1;
         for (int64_t I = I0; I < std::min(ihi, I0 + sr); ++I) {
           if (train && I * rb >= jmax) break;
-          if (t++ % world == rank) tiles.push_back(make_int2((int)I, (int)J));
+          if ((by_band ? I : t) % world == rank) tiles.push_back(make_int2((int)I, (int)J));
+          ++t;
         }
       }
     }
@@ -709,7 +726,7 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
       band_tiles.push_back((int64_t)tiles.size());
     }
   } else {
-    tiles = make_tiles(train, a.n_bras, a.n_kets, kWarpsO1, kLanes, a.rank, a.world);
+    tiles = make_tiles(train, a.n_bras, a.n_kets, kWarpsO1, kLanes, a.rank, a.world, 0, -1, a.rows_out != nullptr);
     band_rows.push_back(a.n_bras);
     band_tiles.push_back((int64_t)tiles.size());
   }
@@ -773,6 +790,14 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
             static_cast<const int32_t*>(kinv), train, a.host_out, a.ld);
       e = cudaGetLastError();
     }
+    // A failed launch part-way through: bands already queued may still write
+    // into the caller's host K, so drain every stream before reporting it
+    // (the caller may free or reuse K_out as soon as it sees the error).
+    if (e != cudaSuccess) {
+      cudaStreamSynchronize(st);
+      cudaStreamSynchronize(alt);
+      cudaStreamSynchronize(side);
+    }
     // join: the main stream (and the buffer frees below) wait for both
     if (evs[bands + 2]) {
       cudaEventRecord(evs[bands + 1], alt);
@@ -810,7 +835,15 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
     overlap_o1_kernel<<<grid, kWarpsO1 * 32, smem, st>>>(o);
     const int32_t* bpos = train ? static_cast<const int32_t*>(kinv) : nullptr;
     const int rows = (int)std::min<int64_t>(a.n_bras, 148 * 32);
-    if (a.out_mode == MPSKQ_OUT_KERNEL)
+    if (a.rows_out) {
+      const int64_t n_owned = owned_row_count(4, a.n_bras, a.rank, a.world);
+      if (n_owned > 0)
+        owned_rows_kernel<<<(int)std::min<int64_t>(n_owned, 148 * 32), 256, 0, st>>>(
+            static_cast<const double*>(ordered), a.n_bras, a.n_kets, kWarpsO1, a.rank, a.world,
+            train ? kperm : nullptr, static_cast<const int32_t*>(kinv), a.rows_out, a.row_ids_out, n_owned);
+      if (a.ket_pos_out)
+        cudaMemcpyAsync(a.ket_pos_out, kinv, sizeof(int32_t) * a.n_kets, cudaMemcpyDeviceToDevice, st);
+    } else if (a.out_mode == MPSKQ_OUT_KERNEL)
       unpermute_kernel<double><<<rows, 256, 0, st>>>(static_cast<const double*>(ordered), a.n_kets, bpos,
                                                      static_cast<const int32_t*>(kinv), a.n_bras, a.out, a.ld);
     else
@@ -834,9 +867,14 @@ int launch_mma(const OverlapArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(mma)");
   }
   const bool train = a.kind == MPSKQ_KIND_TRAIN;
-  auto tiles = make_tiles(train, a.n_bras, a.n_kets, 1, C::pairs, a.rank, a.world);
+  auto tiles = make_tiles(train, a.n_bras, a.n_kets, 1, C::pairs, a.rank, a.world, 0, -1, a.rows_out != nullptr);
   int2* dtiles = nullptr;
   if (int s = upload_tiles(tiles, &dtiles, st)) return s;
+  double* full = nullptr;  // row ownership: the rank's rows in a full-size buffer, then compacted
+  if (a.rows_out) {
+    e = cudaMallocAsync(reinterpret_cast<void**>(&full), sizeof(double) * std::max<int64_t>(1, a.n_bras * a.n_kets), st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(owned rows)");
+  }
   if (!tiles.empty()) {
     MmaArgs o{reinterpret_cast<const double2*>(a.bra_sites),
               reinterpret_cast<const double2*>(a.ket_sites),
@@ -851,8 +889,8 @@ int launch_mma(const OverlapArgs& a, cudaStream_t st) {
               a.out_mode,
               dtiles,
               (int64_t)tiles.size(),
-              a.out,
-              a.ld,
+              full ? full : a.out,
+              full ? a.n_kets : a.ld,
               nullptr};
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -865,6 +903,13 @@ int launch_mma(const OverlapArgs& a, cudaStream_t st) {
     }
     overlap_mma_kernel<CAP><<<grid, C::warps * 32, C::smem, st>>>(o);
     if (o.gws) cudaFreeAsync(o.gws, st);
+  }
+  if (full) {
+    const int64_t n_owned = owned_row_count(CAP, a.n_bras, a.rank, a.world);
+    if (n_owned > 0)
+      owned_rows_kernel<<<(int)std::min<int64_t>(n_owned, 148 * 32), 256, 0, st>>>(
+          full, a.n_bras, a.n_kets, 1, a.rank, a.world, nullptr, nullptr, a.rows_out, a.row_ids_out, n_owned);
+    cudaFreeAsync(full, st);
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "overlap_mma launch");
@@ -893,13 +938,81 @@ int launch_overlap(const OverlapArgs& a, void* stream) {
     default: return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", a.chi_cap);
   }
   if (s != MPSKQ_OK) return s;
-  if (a.kind == MPSKQ_KIND_TRAIN && a.out_mode == MPSKQ_OUT_KERNEL && a.rank == 0 &&
+  if (a.kind == MPSKQ_KIND_TRAIN && a.out_mode == MPSKQ_OUT_KERNEL && a.rank == 0 && !a.rows_out &&
       !(a.host_out && a.chi_cap == 4 && a.world == 1)) {
     fill_diag_kernel<<<(int)std::min<int64_t>((a.n_bras + 255) / 256, 1024), 256, 0, st>>>(
         a.out, a.ld, a.n_bras);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "fill_diag launch");
   }
+  return MPSKQ_OK;
+}
+
+int64_t owned_row_count(int chi_cap, int64_t n_bras, int rank, int world) {
+  const int64_t rb = chi_cap == 4 ? kWarpsO1 : 1;
+  const int64_t nbands = (n_bras + rb - 1) / rb;
+  int64_t n = 0;
+  for (int64_t b = rank; b < nbands; b += world) n += std::min<int64_t>(rb, n_bras - b * rb);
+  // compact indexing assumes full bands before the last one of this rank
+  return n == 0 ? 0 : ((n + rb - 1) / rb) * rb;
+}
+
+// Gatherer side of row ownership: scatter the ranks' compact rows into K
+// (caller order) and, for the train kind, complete every entry whose row was
+// not the computing one: K[a][b] = K[b][a] when pos[b] < pos[a] (pos = the
+// ordered position, identity without one); unit diagonal.  32x32 tiles
+// through shared memory keep both reads coalesced.
+__global__ void scatter_rows_kernel(const double* __restrict__ rows, const int32_t* __restrict__ ids,
+                                    int64_t n_rows, int64_t nk, double* __restrict__ K, int64_t ld) {
+  for (int64_t k = blockIdx.x; k < n_rows; k += gridDim.x) {
+    const int32_t a = ids[k];
+    if (a < 0) continue;
+    for (int64_t b = threadIdx.x; b < nk; b += blockDim.x) K[(int64_t)a * ld + b] = rows[k * nk + b];
+  }
+}
+
+__global__ void mirror_by_pos_kernel(double* __restrict__ K, int64_t n, int64_t ld,
+                                     const int32_t* __restrict__ pos) {
+  __shared__ double t1[32][33], t2[32][33];
+  const int64_t nt = (n + 31) / 32;
+  for (int64_t tile = blockIdx.x; tile < nt * nt; tile += gridDim.x) {
+    const int64_t A = tile / nt, B = tile % nt;
+    if (A > B) continue;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+    for (int r = ty; r < 32; r += 8) {
+      const int64_t a = A * 32 + r, b = B * 32 + tx;
+      t1[r][tx] = (a < n && b < n) ? K[a * ld + b] : 0.0;  // block (A, B)
+      const int64_t a2 = B * 32 + r, b2 = A * 32 + tx;
+      t2[r][tx] = (a2 < n && b2 < n) ? K[a2 * ld + b2] : 0.0;  // block (B, A)
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+      // (a, b) in block (A, B): a = A*32 + r, b = B*32 + tx
+      const int64_t a = A * 32 + r, b = B * 32 + tx;
+      if (a < n && b < n) {
+        const int pa = pos ? pos[a] : (int)a, pb = pos ? pos[b] : (int)b;
+        K[a * ld + b] = a == b ? 1.0 : (pa < pb ? t1[r][tx] : t2[tx][r]);
+      }
+      const int64_t a2 = B * 32 + r, b2 = A * 32 + tx;
+      if (a2 < n && b2 < n) {
+        const int pa = pos ? pos[a2] : (int)a2, pb = pos ? pos[b2] : (int)b2;
+        K[a2 * ld + b2] = a2 == b2 ? 1.0 : (pa < pb ? t2[r][tx] : t1[tx][r]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+int assemble_rows(int kind, int64_t n_bras, int64_t n_kets, const double* rows, const int32_t* ids, int64_t n_rows,
+                  const int32_t* ket_pos, double* K, int64_t ld, cudaStream_t st) {
+  if (n_rows > 0)
+    scatter_rows_kernel<<<(int)std::min<int64_t>(n_rows, 148 * 32), 256, 0, st>>>(rows, ids, n_rows, n_kets, K, ld);
+  if (kind == MPSKQ_KIND_TRAIN && n_bras > 0) {
+    const int64_t nt = (n_bras + 31) / 32;
+    mirror_by_pos_kernel<<<(int)std::min<int64_t>(nt * nt, 148 * 16), 256, 0, st>>>(K, n_bras, ld, ket_pos);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "assemble_rows launch");
   return MPSKQ_OK;
 }
 
@@ -945,4 +1058,68 @@ extern "C" int mpskq_overlap_tiles(int kind, int chi_cap, int64_t n_bras, int64_
     tiles[2 * i + 1] = t[i].y;
   }
   return MPSKQ_OK;
+}
+
+extern "C" int mpskq_owned_rows(int chi_cap, int64_t n_bras, int rank, int world, int64_t* n_owned) {
+  using namespace mpskq;
+  if (!chi_cap_supported(chi_cap))
+    return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", chi_cap);
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(MPSKQ_ERR_INVALID, "bad rank %d of world %d", rank, world);
+  if (n_bras < 0) return fail(MPSKQ_ERR_INVALID, "negative state counts");
+  if (n_owned) *n_owned = owned_row_count(chi_cap, n_bras, rank, world);
+  return MPSKQ_OK;
+}
+
+extern "C" int mpskq_overlap_owned_rows(int kind, int m, int chi_cap, const int64_t* site_off_dev,
+                                        int64_t state_stride, const double* bra_sites_dev,
+                                        const int32_t* bra_chi_dev, int64_t n_bras, const double* ket_sites_dev,
+                                        const int32_t* ket_chi_dev, int64_t n_kets, int rank, int world,
+                                        double* rows_out_dev, int32_t* row_ids_dev, int32_t* ket_pos_dev,
+                                        void* stream) {
+  using namespace mpskq;
+  if (kind != MPSKQ_KIND_TRAIN && kind != MPSKQ_KIND_TEST)
+    return fail(MPSKQ_ERR_INVALID, "kind must be one of ('train', 'test')");
+  if (!chi_cap_supported(chi_cap))
+    return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", chi_cap);
+  if (kind == MPSKQ_KIND_TRAIN &&
+      (n_bras != n_kets || bra_sites_dev != ket_sites_dev || bra_chi_dev != ket_chi_dev))
+    return fail(MPSKQ_ERR_INVALID, "train kind requires bras and kets to be the same states");
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(MPSKQ_ERR_INVALID, "bad rank %d of world %d", rank, world);
+  if (!rows_out_dev || !row_ids_dev) return fail(MPSKQ_ERR_INVALID, "owned-row outputs are required");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t n_owned = owned_row_count(chi_cap, n_bras, rank, world);
+  if (n_owned > 0) {
+    // padding rows of a short last band keep id -1 (skipped by the scatter)
+    cudaError_t e = cudaMemsetAsync(row_ids_dev, 0xff, sizeof(int32_t) * n_owned, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(row ids)");
+  }
+  if (ket_pos_dev && chi_cap != 4) {
+    std::vector<int32_t> id(n_kets);
+    for (int64_t i = 0; i < n_kets; ++i) id[i] = (int32_t)i;
+    cudaError_t e = cudaMemcpyAsync(ket_pos_dev, id.data(), sizeof(int32_t) * n_kets, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "ket positions");
+  }
+  if (n_bras == 0 || n_kets == 0) return MPSKQ_OK;
+  OverlapArgs a{kind, MPSKQ_OUT_KERNEL, m, chi_cap, site_off_dev, state_stride, bra_sites_dev, bra_chi_dev,
+                n_bras, ket_sites_dev, ket_chi_dev, n_kets, rank, world, nullptr, n_kets};
+  a.rows_out = rows_out_dev;
+  a.row_ids_out = row_ids_dev;
+  a.ket_pos_out = ket_pos_dev;
+  return launch_overlap(a, stream);
+}
+
+extern "C" int mpskq_assemble_rows(int kind, int64_t n_bras, int64_t n_kets, const double* rows_dev,
+                                   const int32_t* row_ids_dev, int64_t n_rows, const int32_t* ket_pos_dev,
+                                   double* K_dev, int64_t ld, void* stream) {
+  using namespace mpskq;
+  if (kind != MPSKQ_KIND_TRAIN && kind != MPSKQ_KIND_TEST)
+    return fail(MPSKQ_ERR_INVALID, "kind must be one of ('train', 'test')");
+  if (kind == MPSKQ_KIND_TRAIN && n_bras != n_kets)
+    return fail(MPSKQ_ERR_INVALID, "train kind requires a square matrix");
+  if (ld < n_kets || n_rows < 0) return fail(MPSKQ_ERR_INVALID, "bad assembly sizes");
+  return assemble_rows(kind, n_bras, n_kets, rows_dev, row_ids_dev, n_rows, ket_pos_dev, K_dev, ld,
+                       static_cast<cudaStream_t>(stream));
 }

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <tuple>
 #include <vector>
@@ -349,6 +350,50 @@ int mpskq_simulate(int m, int chi_cap, const int32_t* ops_dev, int64_t n_ops, in
   return launch_simulate(a, stream);
 }
 
+int mpskq_run_program(int m, int chi_cap, const int32_t* ops_dev, int64_t n_ops, int64_t n_gates,
+                      const double* coef_dev, int64_t n_params, int64_t n_states, double budget,
+                      int chi_max, const int64_t* site_off_dev, int64_t state_stride,
+                      int from_input, double* sites_dev, int32_t* chi_dev, double* discard_dev,
+                      int32_t* peak_chi_dev, int32_t* status_dev, int64_t* entry_log_dev,
+                      int64_t* phase_cycles_dev, void* stream) {
+  if (m < 1) return fail(MPSKQ_ERR_INVALID, "qubit count must be at least 1");
+  if (!chi_cap_supported(chi_cap))
+    return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", chi_cap);
+  if (!(budget >= 0)) return fail(MPSKQ_ERR_INVALID, "budget must be non-negative");
+  if (n_states < 0 || n_ops < 0) return fail(MPSKQ_ERR_INVALID, "negative sizes");
+  if (n_states == 0) return MPSKQ_OK;
+  SimArgs a{m,        chi_cap,  ops_dev,      n_ops,        n_gates,   coef_dev,
+            n_params, n_states, budget,       chi_max,      site_off_dev, state_stride,
+            sites_dev, chi_dev, discard_dev,  peak_chi_dev, status_dev, entry_log_dev, nullptr};
+  a.from_input = from_input != 0;
+  a.phase_cycles = reinterpret_cast<long long*>(phase_cycles_dev);
+  return launch_simulate(a, stream);
+}
+
+int mpskq_relayout(int m, int64_t n, const double* src_sites_dev, const int64_t* src_off_dev,
+                   int64_t src_stride, const int32_t* chi_dev, double* dst_sites_dev,
+                   const int64_t* dst_off_dev, int64_t dst_stride, const int32_t* dst_rows_dev,
+                   void* stream) {
+  if (m < 1 || n < 0) return fail(MPSKQ_ERR_INVALID, "bad relayout sizes");
+  return launch_relayout(m, n, src_sites_dev, src_off_dev, src_stride, chi_dev, dst_sites_dev, dst_off_dev,
+                         dst_stride, dst_rows_dev, stream);
+}
+
+int mpskq_pack_exact(int m, int64_t n, const double* sites_dev, const int64_t* site_off_dev, int64_t state_stride,
+                     const int32_t* chi_dev, const int64_t* state_off_dev, double* packed_dev, void* stream) {
+  if (m < 1 || n < 0) return fail(MPSKQ_ERR_INVALID, "bad pack sizes");
+  return launch_pack_exact(m, n, const_cast<double*>(sites_dev), site_off_dev, state_stride, chi_dev, state_off_dev,
+                           packed_dev, 0, stream);
+}
+
+int mpskq_unpack_exact(int m, int64_t n, const double* packed_dev, const int64_t* state_off_dev,
+                       const int32_t* chi_dev, double* sites_dev, const int64_t* site_off_dev, int64_t state_stride,
+                       void* stream) {
+  if (m < 1 || n < 0) return fail(MPSKQ_ERR_INVALID, "bad unpack sizes");
+  return launch_pack_exact(m, n, sites_dev, site_off_dev, state_stride, chi_dev, state_off_dev,
+                           const_cast<double*>(packed_dev), 1, stream);
+}
+
 int mpskq_svd_truncated_batched(int rows, int cols, int64_t batch, const double* mats_dev,
                                 double budget, int chi_max, double* u_dev, double* s_dev,
                                 double* vh_dev, int32_t* keep_dev, double* discarded_dev,
@@ -388,6 +433,15 @@ int mpskq_overlap(int kind, int out_mode, int m, int chi_cap, const int64_t* sit
                 bra_sites_dev, bra_chi_dev, n_bras, ket_sites_dev, ket_chi_dev,  n_kets,
                 rank,     world,         out_dev,  ld};
   return launch_overlap(a, stream);
+}
+
+int mpskq_sm_clock_khz(void) {
+  int dev = 0, khz = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return khz;
 }
 
 int mpskq_fp64_probe(int n_blocks, int64_t iters, double* out_dev, void* stream) {
@@ -483,6 +537,47 @@ int check_rows_host(const double* X, int64_t n, int m) {
   return MPSKQ_OK;
 }
 
+// K of the given device states into host memory K_out (n_bras x n_kets).
+// Pinned (page-locked, device-mapped) K_out on the chi <= 4 path: the
+// overlap streams finished row bands straight into it while later bands
+// compute, so the 8 B/entry device->host transfer hides under the overlap.
+// Pageable K_out: device K, then one copy.  ev_done (nullable) is recorded
+// when the overlap kernels are queued.  Does not synchronise.
+int overlap_into_host(int kind, int m, int cap, const int64_t* doff, int64_t stride, const double* bra_sites,
+                      const int32_t* bra_chi, int64_t n_bras, const double* ket_sites, const int32_t* ket_chi,
+                      int64_t n_kets, double* K_out, void* stream, cudaEvent_t ev_done) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* k_mapped = nullptr;
+  if (cap == 4 && n_bras > 0 && n_kets > 0) {
+    cudaPointerAttributes pa{};
+    int cur = 0;
+    cudaGetDevice(&cur);
+    // only a buffer registered by this device's context is safely mapped here
+    // (a buffer pinned by another device without cudaHostAllocPortable is not)
+    if (cudaPointerGetAttributes(&pa, K_out) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer && pa.device == cur)
+      k_mapped = static_cast<double*>(pa.devicePointer);
+    cudaGetLastError();  // a pageable pointer may leave a sticky-free error behind
+  }
+  if (k_mapped) {
+    OverlapArgs a{kind,      MPSKQ_OUT_KERNEL, m,      cap,       doff,    stride,
+                  bra_sites, bra_chi,          n_bras, ket_sites, ket_chi, n_kets,
+                  0,         1,                nullptr, n_kets};
+    a.host_out = k_mapped;
+    ST(launch_overlap(a, stream));
+    if (ev_done) CK(cudaEventRecord(ev_done, st));
+    return MPSKQ_OK;
+  }
+  AsyncBuf dK;
+  ST(dK.alloc(sizeof(double) * n_bras * n_kets, st));
+  ST(mpskq_overlap(kind, MPSKQ_OUT_KERNEL, m, cap, doff, stride, bra_sites, bra_chi, n_bras, ket_sites, ket_chi,
+                   n_kets, 0, 1, dK.as<double>(), n_kets, stream));
+  if (ev_done) CK(cudaEventRecord(ev_done, st));
+  if (n_bras * n_kets)
+    CK(cudaMemcpyAsync(K_out, dK.p, sizeof(double) * n_bras * n_kets, cudaMemcpyDeviceToHost, st));
+  return MPSKQ_OK;
+}
+
 }  // namespace
 
 extern "C" int mpskq_gram_host(int kind, int m, int r, int d, double gamma, double budget,
@@ -548,7 +643,10 @@ extern "C" int mpskq_gram_host(int kind, int m, int r, int d, double gamma, doub
   CK(cudaMemsetAsync(dbad.p, 0, sizeof(int), st));
   ST(launch_encode(dX.as<double>(), n_all, m, r, d, gamma, dcoef.as<double>(), dbad.as<int>(), st));
 
-  // simulate every state once, escalating the chi capacity on overflow
+  // Simulate every state at the hinted capacity; states that outgrow it (and
+  // only those) are re-simulated at the next capacity, and so on (per-state
+  // escalation).  The levels are then gathered into the final capacity's
+  // layout, so the overlap sees one batch.
   const auto key = std::make_tuple(m, r, d, budget, chi_max);
   int cap_idx = 0;
   if (chi_cap) {
@@ -558,43 +656,90 @@ extern "C" int mpskq_gram_host(int kind, int m, int r, int d, double gamma, doub
     auto it = cache().cap_hint.find(key);
     if (it != cache().cap_hint.end()) cap_idx = it->second;
   }
-  AsyncBuf sites, chi, disc, peak, status, doff;
-  int64_t stride = 0;
-  int cap = 0;
-  std::vector<int32_t> hstatus(n_all);
+  struct Level {
+    int cap_idx = 0;
+    int64_t n = 0, stride = 0;
+    AsyncBuf sites, chi, disc, peak, status, doff, rows, coef;
+  };
+  std::vector<std::unique_ptr<Level>> levels;
+  std::vector<int32_t> todo;  // global rows still to simulate (empty = all, level 0)
+  std::vector<int64_t> counts;
   for (;; ++cap_idx) {
     if (cap_idx >= kNumChiCaps)
       return fail(MPSKQ_ERR_CAPACITY, "bond dimension exceeds the largest compiled capacity %d",
                   kChiCaps[kNumChiCaps - 1]);
-    cap = kChiCaps[cap_idx];
+    auto L = std::make_unique<Level>();
+    L->cap_idx = cap_idx;
+    L->n = levels.empty() ? n_all : (int64_t)todo.size();
+    const int cap_l = kChiCaps[cap_idx];
     std::vector<int64_t> off(m + 1);
-    ST(mpskq_batch_layout(m, cap, off.data(), &stride));
-    for (AsyncBuf* b : {&sites, &chi, &disc, &peak, &status, &doff}) b->reset();
-    ST(doff.alloc(sizeof(int64_t) * (m + 1), st));
-    CK(cudaMemcpyAsync(doff.p, off.data(), sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice, st));
+    ST(mpskq_batch_layout(m, cap_l, off.data(), &L->stride));
+    ST(L->doff.alloc(sizeof(int64_t) * (m + 1), st));
+    CK(cudaMemcpyAsync(L->doff.p, off.data(), sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice, st));
+    const double* coef_l = dcoef.as<double>();
+    if (!levels.empty()) {
+      ST(L->rows.alloc(sizeof(int32_t) * L->n, st));
+      CK(cudaMemcpyAsync(L->rows.p, todo.data(), sizeof(int32_t) * L->n, cudaMemcpyHostToDevice, st));
+      ST(L->coef.alloc(sizeof(double) * 2 * n_params * L->n, st));
+      ST(launch_copy_rows(dcoef.p, L->coef.p, sizeof(double) * 2 * n_params, L->n, L->rows.as<int32_t>(),
+                          nullptr, st));
+      coef_l = L->coef.as<double>();
+    }
+    ST(L->sites.alloc(sizeof(double) * 2 * L->stride * L->n, st));
+    ST(L->chi.alloc(sizeof(int32_t) * (m + 1) * L->n, st));
+    ST(L->disc.alloc(sizeof(double) * L->n, st));
+    ST(L->peak.alloc(sizeof(int32_t) * L->n, st));
+    ST(L->status.alloc(sizeof(int32_t) * L->n, st));
+    ST(mpskq_simulate(m, cap_l, dops.as<int32_t>(), n_ops, n_gates, coef_l, n_params, L->n, budget, chi_max,
+                      L->doff.as<int64_t>(), L->stride, L->sites.as<double>(), L->chi.as<int32_t>(),
+                      L->disc.as<double>(), L->peak.as<int32_t>(), L->status.as<int32_t>(), nullptr, stream));
+    std::vector<int32_t> hstatus(L->n);
+    CK(cudaMemcpyAsync(hstatus.data(), L->status.p, sizeof(int32_t) * L->n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<int32_t> next;
+    for (int64_t i = 0; i < L->n; ++i) {
+      if (hstatus[i] == MPSKQ_STATE_NONFINITE) return fail(MPSKQ_ERR_NUMERIC, "tensor has non-finite entries");
+      if (hstatus[i] == MPSKQ_STATE_NOCONV) return fail(MPSKQ_ERR_NUMERIC, "SVD did not converge");
+      if (hstatus[i] == MPSKQ_STATE_CAPACITY) next.push_back(levels.empty() ? (int32_t)i : todo[i]);
+    }
+    counts.push_back(L->n);
+    levels.push_back(std::move(L));
+    if (next.empty()) break;
+    if (chi_cap) return fail(MPSKQ_ERR_CAPACITY, "bond dimension exceeds chi capacity %d", kChiCaps[cap_idx]);
+    todo.swap(next);
+  }
+  if (!chi_cap) {
+    // next call starts at the first level that held >= 7/8 of the states
+    size_t h = 0;
+    while (h + 1 < counts.size() && counts[h + 1] * 8 > n_all) ++h;
+    std::lock_guard<std::mutex> g(cache().mu);
+    cache().cap_hint[key] = levels[h]->cap_idx;
+  }
+  Level& fin = *levels.back();
+  const int cap = kChiCaps[fin.cap_idx];
+  const int64_t stride = fin.stride;
+  AsyncBuf sites, chi, disc, peak, doff;
+  if (levels.size() == 1) {
+    std::swap(sites.p, fin.sites.p);
+    std::swap(chi.p, fin.chi.p);
+    std::swap(doff.p, fin.doff.p);
+    sites.st = chi.st = doff.st = st;
+  } else {
     ST(sites.alloc(sizeof(double) * 2 * stride * n_all, st));
     ST(chi.alloc(sizeof(int32_t) * (m + 1) * n_all, st));
     ST(disc.alloc(sizeof(double) * n_all, st));
     ST(peak.alloc(sizeof(int32_t) * n_all, st));
-    ST(status.alloc(sizeof(int32_t) * n_all, st));
-    ST(mpskq_simulate(m, cap, dops.as<int32_t>(), n_ops, n_gates, dcoef.as<double>(), n_params, n_all,
-                      budget, chi_max, doff.as<int64_t>(), stride, sites.as<double>(),
-                      chi.as<int32_t>(), disc.as<double>(), peak.as<int32_t>(),
-                      status.as<int32_t>(), nullptr, stream));
-    CK(cudaMemcpyAsync(hstatus.data(), status.p, sizeof(int32_t) * n_all, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    bool overflow = false;
-    for (int32_t s : hstatus) {
-      if (s == MPSKQ_STATE_NONFINITE)
-        return fail(MPSKQ_ERR_NUMERIC, "tensor has non-finite entries");
-      overflow |= s == MPSKQ_STATE_CAPACITY;
+    std::swap(doff.p, fin.doff.p);
+    doff.st = st;
+    for (auto& Lp : levels) {  // later levels overwrite the rows that overflowed earlier ones
+      Level& L = *Lp;
+      const int32_t* rows = L.rows.p ? L.rows.as<int32_t>() : nullptr;
+      ST(launch_relayout(m, L.n, L.sites.as<double>(), L.doff.p ? L.doff.as<int64_t>() : doff.as<int64_t>(),
+                         L.stride, L.chi.as<int32_t>(), sites.as<double>(), doff.as<int64_t>(), stride, rows, st));
+      ST(launch_copy_rows(L.chi.p, chi.p, sizeof(int32_t) * (m + 1), L.n, nullptr, rows, st));
+      ST(launch_copy_rows(L.disc.p, disc.p, sizeof(double), L.n, nullptr, rows, st));
+      ST(launch_copy_rows(L.peak.p, peak.p, sizeof(int32_t), L.n, nullptr, rows, st));
     }
-    if (!overflow) break;
-    if (chi_cap) return fail(MPSKQ_ERR_CAPACITY, "bond dimension exceeds chi capacity %d", cap);
-  }
-  if (!chi_cap) {
-    std::lock_guard<std::mutex> g(cache().mu);
-    cache().cap_hint[key] = cap_idx;
   }
   CK(cudaEventRecord(ev[1], st));
 
@@ -602,34 +747,8 @@ extern "C" int mpskq_gram_host(int kind, int m, int r, int d, double gamma, doub
   const int32_t* bra_chi = chi.as<int32_t>();
   const double* ket_sites = train ? bra_sites : bra_sites + 2 * stride * n_bras;
   const int32_t* ket_chi = train ? bra_chi : bra_chi + (m + 1) * n_bras;
-  // Pinned (page-locked, device-mapped) K_out on the chi <= 4 path: the
-  // overlap streams finished row bands straight into it while later bands
-  // compute, so the 8 B/entry device->host transfer hides under the overlap.
-  // Pageable K_out: device K, then one copy.
-  double* k_mapped = nullptr;
-  if (cap == 4 && n_bras > 0 && n_kets > 0) {
-    cudaPointerAttributes pa{};
-    if (cudaPointerGetAttributes(&pa, K_out) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
-        pa.devicePointer)
-      k_mapped = static_cast<double*>(pa.devicePointer);
-    cudaGetLastError();  // a pageable pointer may leave a sticky-free error behind
-  }
-  AsyncBuf dK;
-  if (k_mapped) {
-    OverlapArgs a{kind,      MPSKQ_OUT_KERNEL, m,      cap,       doff.as<int64_t>(), stride,
-                  bra_sites, bra_chi,          n_bras, ket_sites, ket_chi,            n_kets,
-                  0,         1,                nullptr, n_kets};
-    a.host_out = k_mapped;
-    ST(launch_overlap(a, stream));
-    CK(cudaEventRecord(ev[2], st));
-  } else {
-    ST(dK.alloc(sizeof(double) * n_bras * n_kets, st));
-    ST(mpskq_overlap(kind, MPSKQ_OUT_KERNEL, m, cap, doff.as<int64_t>(), stride, bra_sites, bra_chi,
-                     n_bras, ket_sites, ket_chi, n_kets, 0, 1, dK.as<double>(), n_kets, stream));
-    CK(cudaEventRecord(ev[2], st));
-    if (n_bras * n_kets)
-      CK(cudaMemcpyAsync(K_out, dK.p, sizeof(double) * n_bras * n_kets, cudaMemcpyDeviceToHost, st));
-  }
+  ST(overlap_into_host(kind, m, cap, doff.as<int64_t>(), stride, bra_sites, bra_chi, n_bras, ket_sites, ket_chi,
+                       n_kets, K_out, stream, ev[2]));
   CK(cudaEventRecord(ev[3], st));
   CK(cudaStreamSynchronize(st));
   if (seconds) {
@@ -642,5 +761,24 @@ extern "C" int mpskq_gram_host(int kind, int m, int r, int d, double gamma, doub
     seconds[2] = 0.0;
     seconds[3] = 1e-3 * t23;
   }
+  return MPSKQ_OK;
+}
+
+extern "C" int mpskq_overlap_host(int kind, int m, int chi_cap, const int64_t* site_off_dev,
+                                  int64_t state_stride, const double* bra_sites_dev, const int32_t* bra_chi_dev,
+                                  int64_t n_bras, const double* ket_sites_dev, const int32_t* ket_chi_dev,
+                                  int64_t n_kets, double* K_out, void* stream) {
+  if (kind != MPSKQ_KIND_TRAIN && kind != MPSKQ_KIND_TEST)
+    return fail(MPSKQ_ERR_INVALID, "kind must be one of ('train', 'test')");
+  if (!chi_cap_supported(chi_cap))
+    return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", chi_cap);
+  if (kind == MPSKQ_KIND_TRAIN &&
+      (n_bras != n_kets || bra_sites_dev != ket_sites_dev || bra_chi_dev != ket_chi_dev))
+    return fail(MPSKQ_ERR_INVALID, "train kind requires bras and kets to be the same states");
+  if (n_bras < 0 || n_kets < 0) return fail(MPSKQ_ERR_INVALID, "negative state counts");
+  if (n_bras == 0 || n_kets == 0) return MPSKQ_OK;
+  ST(overlap_into_host(kind, m, chi_cap, site_off_dev, state_stride, bra_sites_dev, bra_chi_dev, n_bras,
+                       ket_sites_dev, ket_chi_dev, n_kets, K_out, stream, nullptr));
+  CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   return MPSKQ_OK;
 }

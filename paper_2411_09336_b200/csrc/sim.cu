@@ -19,6 +19,7 @@
 // values the truncation rule compares against the budget.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cfloat>
 
 #include "device.cuh"
@@ -31,6 +32,7 @@ __device__ constexpr double kNoiseFloor = 10.0 * DBL_EPSILON;
 // 1/sqrt(2) exactly as the reference rounds it: _H_MATRIX = [[1,1],[1,-1]]/sqrt(2)
 __device__ constexpr double kInvSqrt2 = 0.7071067811865475;
 constexpr int kMaxSweeps = 40;
+constexpr int kNoConvergence = 1 << 30;  // flag bit in jacobi()'s round count
 // Lanes (threads) per state by capacity.  Same-box A/B of the simulator
 // (tools/ab_sim_headline.py, tools/ab_sim_cfg.py, tools/ab_sim.py): halving
 // the old 16/64/128/256/384 sped up capacity 4 (15.6 -> 13.7 ms at the
@@ -568,14 +570,17 @@ __device__ __noinline__ int jacobi_sweeps(Smem<CAP, NT>& sm, int Rr, int n) {
   // most |c_small|^2 <= (5 eps s0)^2 -- far below the LAPACK-vs-Jacobi
   // rounding already present -- but rotating on their rounding noise was what
   // kept large thetas sweeping (measured 12-15 sweeps at chi 17-44).
-  // ||theta||_F^2 / 4 * eps^2 <= (5 eps s0)^2 for n <= 100 columns.
+  // With n columns ||theta||_F^2 <= n s0^2, so the threshold
+  // eps^2 ||theta||_F^2 / 4 * min(1, 100 / n) stays <= (5 eps s0)^2 for any n
+  // (up to the 256 columns of capacity 128).
   double fro = 0.0;
   #pragma unroll 1
   for (int idx = tid; idx < Rr * n; idx += NT) {
     const int c = idx / Rr, r = idx - c * Rr;
     fro += cnorm2(A[c * LD + r]);
   }
-  const double noise2 = 0.25 * DBL_EPSILON * DBL_EPSILON * block_sum<NT>(fro, sm.red);
+  const double noise2 =
+      0.25 * DBL_EPSILON * DBL_EPSILON * block_sum<NT>(fro, sm.red) * (n > 100 ? 100.0 / n : 1.0);
   int round = 0, quiet = 0;
   for (; round < max_rounds;) {
     const int t = round % span;
@@ -655,9 +660,9 @@ __device__ __noinline__ int jacobi_sweeps(Smem<CAP, NT>& sm, int Rr, int n) {
     }
     ++round;
     quiet = block_any<NT>(rot) ? 0 : quiet + 1;
-    if (quiet >= span) break;
+    if (quiet >= span) return round;
   }
-  return round;
+  return round | kNoConvergence;  // no quiet cycle within kMaxSweeps sweeps
 }
 
 // Log mode: W = I_n in `Wm`, then apply the logged rotations in order.
@@ -808,7 +813,8 @@ struct StateCtx {
 };
 
 template <int CAP, int NT>
-__device__ void op_one_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, double2 cs) {
+__device__ void op_one_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, double2 cs,
+                             const double2* gm) {
   const int chl = sm.chi[q], chr = sm.chi[q + 1];
   double2* p = st.base + st.off[q];
   const int n = chl * chr;
@@ -817,7 +823,13 @@ __device__ void op_one_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, d
     const int a = idx / chr, b = idx - a * chr;
     const int i0 = (2 * a) * chr + b, i1 = i0 + chr;
     const double2 x0 = p[i0], x1 = p[i1];
-    if (code == MPSKQ_OP_H) {
+    if (code == MPSKQ_OP_U1) {
+      // arbitrary 2x2 matrix U (row-major in the coefficient row):
+      // site <- tensordot(U, site, (1, 1)).transpose(1, 0, 2)  (mps.py:157)
+      const double2 u00 = gm[0], u01 = gm[1], u10 = gm[2], u11 = gm[3];
+      p[i0] = cfma(u01, x1, cmul(u00, x0));
+      p[i1] = cfma(u11, x1, cmul(u10, x0));
+    } else if (code == MPSKQ_OP_H) {
       const double h = kInvSqrt2;
       p[i0] = make_double2(__dadd_rn(__dmul_rn(h, x0.x), __dmul_rn(h, x1.x)),
                            __dadd_rn(__dmul_rn(h, x0.y), __dmul_rn(h, x1.y)));
@@ -916,7 +928,7 @@ __device__ void op_qr_right(Smem<CAP, NT>& sm, StateCtx& st, int i) {
 // apply_two_qubit at (q, q+1) after canonicalize(q) (mps.py:163-205)
 template <int CAP, int NT>
 __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, bool left,
-                             double2 cs, double budget, int chi_max) {
+                             double2 cs, const double2* gm, double budget, int chi_max) {
   constexpr int LD = 2 * CAP;
   const int tid = ltid<NT>();
   const int chl = sm.chi[q], chm = sm.chi[q + 1], chr = sm.chi[q + 2];
@@ -948,8 +960,34 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
   const bool pre = kPrecondition<CAP>::value && kmin >= kPrecondMinCols;
   const bool theta_cm = left != pre;  // store C (not preconditioned) or C^H
   int bad = 0;
+  if (code == MPSKQ_OP_U2) {
+    // arbitrary 4x4 matrix G on |p0 p1> (row-major in the coefficient row):
+    // theta'(l, p0', p1', r) = sum G[p0'p1'][p0 p1] theta(l, p0, p1, r)
+    // (mps.py:184-186); one item per (l, r) couples all four physical entries
+    #pragma unroll 1
+    for (int lr = tid; lr < chl * chr; lr += NT) {
+      const int l = lr / chr, rr = lr - l * chr;
+      double2 T[4] = {cz(), cz(), cz(), cz()};
+      for (int k = 0; k < chm; ++k)
+        #pragma unroll
+        for (int pp = 0; pp < 4; ++pp)
+          T[pp] = cfma(Xs[(2 * l + (pp >> 1)) * chm + k], Ys[k * Nc + (pp & 1) * chr + rr], T[pp]);
+      #pragma unroll
+      for (int po = 0; po < 4; ++po) {
+        double2 o = cz();
+        #pragma unroll
+        for (int pp = 0; pp < 4; ++pp) o = cfma(gm[po * 4 + pp], T[pp], o);
+        bad |= !cfinite(o);
+        const int row = 2 * l + (po >> 1), col = (po & 1) * chr + rr;
+        if (theta_cm)
+          sm.A[col * LD + row] = o;
+        else
+          sm.A[row * LD + col] = cconj(o);
+      }
+    }
+  }
   #pragma unroll 1
-  for (int it = tid; it < chl * chr * 2; it += NT) {
+  for (int it = tid; it < (code == MPSKQ_OP_U2 ? 0 : chl * chr * 2); it += NT) {
     const int t = it & 1, lr = it >> 1;
     const int l = lr / chr, rr = lr - l * chr;
     const int p0a = 0, p1a = t;
@@ -997,7 +1035,11 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
   }
   MPSKQ_DBG_ADD(1, t_qr);
   MPSKQ_DBG_T(t_jac);
-  const int sweeps = jacobi<CAP, NT>(sm, Rr, ncol);
+  int sweeps = jacobi<CAP, NT>(sm, Rr, ncol);
+  if (sweeps & kNoConvergence) {  // LinAlgError in the reference (zgesdd)
+    st.status = MPSKQ_STATE_NOCONV;
+    return;
+  }
   MPSKQ_DBG_ADD(2, t_jac);
   MPSKQ_DBG_T(t_trunc);
 #ifdef MPSKQ_DEBUG_COUNTERS
@@ -1113,7 +1155,18 @@ __global__ void __launch_bounds__(NT * SpcFor<NT>::value) sim_kernel(SimArgs a) 
     bool live = n < a.n_states;  // uniform per state group
     StateCtx st{reinterpret_cast<double2*>(a.sites) + (live ? n : 0) * a.state_stride, a.site_off, m,
                 MPSKQ_STATE_OK, 1, 0.0};
-    if (live) {
+    if (live && a.from_input) {
+      // continue an existing state (apply_gate / canonicalize / run_circuit on
+      // a given MpsState, mps.py:123-247): sites are already in the slab,
+      // bond dims, discard and peak come in through the output arrays
+      #pragma unroll 1
+      for (int b = tid; b <= m; b += NT) sm.chi[b] = a.chi[n * (m + 1) + b];
+      if (tid == 0) {
+        st.discard = a.discard[n];
+        st.peak = a.peak[n];
+      }
+      bsync<NT>();
+    } else if (live) {
       // init_state(m, "zero"): every site (1, 2, 1) = [1, 0]  (mps.py:90-102)
       #pragma unroll 1
       for (int b = tid; b <= m; b += NT) sm.chi[b] = 1;
@@ -1124,6 +1177,8 @@ __global__ void __launch_bounds__(NT * SpcFor<NT>::value) sim_kernel(SimArgs a) 
       }
       bsync<NT>();
     }
+    // per-phase device cycles (MpsState.timings keys, mps.py:137/:159/:204)
+    long long ph_canon = 0, ph_one = 0, ph_two = 0;
     const double2* cf = coef + (live ? n : 0) * a.n_params;
     for (int64_t i = 0; i < a.n_ops; ++i) {
       if (live) {
@@ -1131,10 +1186,13 @@ __global__ void __launch_bounds__(NT * SpcFor<NT>::value) sim_kernel(SimArgs a) 
         const int code = op.x & 0xff;
         const bool left = (op.x >> 8) & MPSKQ_ABSORB_LEFT;
         const double2 cs = op.z >= 0 ? __ldg(cf + op.z) : make_double2(1.0, 0.0);
+        const double2* gm = cf + (op.z >= 0 ? op.z : 0);  // U1 / U2 matrices
+        const long long c0 = a.phase_cycles ? clock64() : 0;
         switch (code) {
           case MPSKQ_OP_H:
           case MPSKQ_OP_RZ:
-            op_one_qubit<CAP, NT>(sm, st, op.y, code, cs);
+          case MPSKQ_OP_U1:
+            op_one_qubit<CAP, NT>(sm, st, op.y, code, cs, gm);
             break;
           case MPSKQ_OP_QRL: {
             MPSKQ_DBG_T(t_mv);
@@ -1149,8 +1207,17 @@ __global__ void __launch_bounds__(NT * SpcFor<NT>::value) sim_kernel(SimArgs a) 
             break;
           }
           default:
-            op_two_qubit<CAP, NT>(sm, st, op.y, code, left, cs, a.budget, a.chi_max);
+            op_two_qubit<CAP, NT>(sm, st, op.y, code, left, cs, gm, a.budget, a.chi_max);
             break;
+        }
+        if (a.phase_cycles) {
+          const long long dt = clock64() - c0;
+          if (code == MPSKQ_OP_QRL || code == MPSKQ_OP_QRR)
+            ph_canon += dt;
+          else if (code == MPSKQ_OP_H || code == MPSKQ_OP_RZ || code == MPSKQ_OP_U1)
+            ph_one += dt;
+          else
+            ph_two += dt;
         }
         if (st.status != MPSKQ_STATE_OK) live = false;  // keep hitting the barriers
         if (live && a.entry_log != nullptr && op.w >= 0 && tid == 0) {
@@ -1168,6 +1235,11 @@ __global__ void __launch_bounds__(NT * SpcFor<NT>::value) sim_kernel(SimArgs a) 
         a.discard[n] = st.discard;
         a.peak[n] = st.peak;
         a.status[n] = st.status;
+        if (a.phase_cycles) {
+          a.phase_cycles[3 * n] = ph_canon;
+          a.phase_cycles[3 * n + 1] = ph_one;
+          a.phase_cycles[3 * n + 2] = ph_two;
+        }
       }
     }
     bsync<NT>();
@@ -1204,7 +1276,12 @@ __global__ void __launch_bounds__(NT) svd_kernel(SvdArgs a) {
       if (tid == 0) a.status[b] = MPSKQ_STATE_NONFINITE;
       continue;
     }
-    const int sweeps = jacobi<CAP, NT>(sm, rows, cols);
+    int sweeps = jacobi<CAP, NT>(sm, rows, cols);
+    if (sweeps & kNoConvergence) {
+      if (tid == 0) a.status[b] = MPSKQ_STATE_NOCONV;
+      bsync<NT>();
+      continue;
+    }
     norms_and_order<CAP, NT>(sm, rows, cols);
     if (tid == 0) truncation_rule<CAP, NT>(sm, kmin, a.budget, a.chi_max);
     bsync<NT>();
@@ -1347,6 +1424,100 @@ int launch_svd(const SvdArgs& a, void* stream) {
   if (big <= 160) return launch_svd_cap<80>(a, st);
   if (big <= 192) return launch_svd_cap<96>(a, st);
   return launch_svd_cap<128>(a, st);
+}
+
+// State relayout between chi-capacity layouts (per-state capacity escalation:
+// the few states that outgrew a capacity are re-simulated at a larger one and
+// everything is gathered into the largest layout).  One CTA per state; every
+// site tensor is (chi_l, 2, chi_r) row-major at the start of its slot in both
+// layouts, so a state moves as m contiguous runs.
+__global__ void relayout_kernel(int m, int64_t n, const double2* __restrict__ src,
+                                const int64_t* __restrict__ src_off, int64_t src_stride,
+                                const int32_t* __restrict__ chi, double2* __restrict__ dst,
+                                const int64_t* __restrict__ dst_off, int64_t dst_stride,
+                                const int32_t* __restrict__ dst_rows) {
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const int32_t* c = chi + i * (m + 1);
+    const double2* s = src + i * src_stride;
+    double2* d = dst + (int64_t)(dst_rows ? dst_rows[i] : i) * dst_stride;
+    for (int site = 0; site < m; ++site) {
+      const int len = 2 * c[site] * c[site + 1];
+      const double2* ss = s + src_off[site];
+      double2* dd = d + dst_off[site];
+      for (int e = threadIdx.x; e < len; e += blockDim.x) dd[e] = ss[e];
+    }
+  }
+}
+
+int launch_relayout(int m, int64_t n, const double* src, const int64_t* src_off, int64_t src_stride,
+                    const int32_t* chi, double* dst, const int64_t* dst_off, int64_t dst_stride,
+                    const int32_t* dst_rows, void* stream) {
+  if (n <= 0) return MPSKQ_OK;
+  relayout_kernel<<<(unsigned)std::min<int64_t>(n, 148 * 16), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      m, n, reinterpret_cast<const double2*>(src), src_off, src_stride, chi, reinterpret_cast<double2*>(dst),
+      dst_off, dst_stride, dst_rows);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "relayout launch");
+  return MPSKQ_OK;
+}
+
+// Exact (unpadded) wire packing of a batch for the multi-GPU exchange: state
+// i's site tensors, (chi_l, 2, chi_r) row-major each, back to back from
+// complex offset state_off[i] (the MPS1 payload order, mps.py:294-314).
+// unpack = 0: layout -> packed; 1: packed -> layout.
+__global__ void pack_exact_kernel(int m, int64_t n, double2* __restrict__ sites, const int64_t* __restrict__ site_off,
+                                  int64_t stride, const int32_t* __restrict__ chi,
+                                  const int64_t* __restrict__ state_off, double2* __restrict__ packed, int unpack) {
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const int32_t* c = chi + i * (m + 1);
+    double2* lay = sites + i * stride;
+    double2* pk = packed + state_off[i];
+    int64_t o = 0;
+    for (int s = 0; s < m; ++s) {
+      const int len = 2 * c[s] * c[s + 1];
+      double2* ls = lay + site_off[s];
+      if (unpack)
+        for (int e = threadIdx.x; e < len; e += blockDim.x) ls[e] = pk[o + e];
+      else
+        for (int e = threadIdx.x; e < len; e += blockDim.x) pk[o + e] = ls[e];
+      o += len;
+    }
+  }
+}
+
+int launch_pack_exact(int m, int64_t n, double* sites, const int64_t* site_off, int64_t stride, const int32_t* chi,
+                      const int64_t* state_off, double* packed, int unpack, void* stream) {
+  if (n <= 0) return MPSKQ_OK;
+  pack_exact_kernel<<<(unsigned)std::min<int64_t>(n, 148 * 16), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      m, n, reinterpret_cast<double2*>(sites), site_off, stride, chi, state_off, reinterpret_cast<double2*>(packed),
+      unpack);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "pack_exact launch");
+  return MPSKQ_OK;
+}
+
+// dst[dst_idx[i]] = src[src_idx[i]] for rows of `words` 32-bit words (either
+// index nullable = identity): coefficient gathers and bond-dim / discard /
+// peak scatters of the per-state capacity escalation
+__global__ void copy_rows_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, int64_t words,
+                                 int64_t n, const int32_t* __restrict__ src_idx,
+                                 const int32_t* __restrict__ dst_idx) {
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const uint32_t* s = src + (int64_t)(src_idx ? src_idx[i] : i) * words;
+    uint32_t* d = dst + (int64_t)(dst_idx ? dst_idx[i] : i) * words;
+    for (int64_t w = threadIdx.x; w < words; w += blockDim.x) d[w] = s[w];
+  }
+}
+
+int launch_copy_rows(const void* src, void* dst, int64_t row_bytes, int64_t n, const int32_t* src_idx,
+                     const int32_t* dst_idx, void* stream) {
+  if (n <= 0) return MPSKQ_OK;
+  if (row_bytes % 4) return fail(MPSKQ_ERR_INVALID, "row size must be a multiple of 4 bytes");
+  copy_rows_kernel<<<(unsigned)std::min<int64_t>(n, 148 * 16), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint32_t*>(src), static_cast<uint32_t*>(dst), row_bytes / 4, n, src_idx, dst_idx);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "copy_rows launch");
+  return MPSKQ_OK;
 }
 
 // FP64 FMA throughput probe: 16 independent DFMA chains per thread

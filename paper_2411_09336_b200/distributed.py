@@ -79,6 +79,94 @@ def allgather_rows(local: torch.Tensor, counts: list, group=None) -> torch.Tenso
     return torch.cat([p[:c] for p, c in zip(parts, counts)], dim=0).to(dev)
 
 
+def exact_offsets(chi: torch.Tensor) -> tuple:
+    """Complex offsets of every state in the exact (unpadded) packing and the
+    total: state i holds sum_s 2 chi_s chi_{s+1} entries (mps.py:61-62)."""
+    ent = (2 * chi[:, :-1].long() * chi[:, 1:].long()).sum(1)
+    return torch.cumsum(ent, 0) - ent, int(ent.sum().item()) if ent.numel() else 0
+
+
+def _pack_native(sites, chi, off, total, m, stride, site_off_dev):
+    from ._device import dptr, stream_ptr
+
+    out = sites.new_empty(max(2 * total, 2))
+    N.check(N.lib().mpskq_pack_exact(m, chi.shape[0], dptr(sites), dptr(site_off_dev), stride, dptr(chi), dptr(off),
+                                     dptr(out), stream_ptr()))
+    return out[: 2 * total]
+
+
+def _unpack_native(packed, off, chi, m, stride, site_off_dev):
+    from ._device import dptr, stream_ptr
+
+    sites = packed.new_empty((chi.shape[0], 2 * stride))
+    N.check(N.lib().mpskq_unpack_exact(m, chi.shape[0], dptr(packed), dptr(off), dptr(chi), dptr(sites),
+                                       dptr(site_off_dev), stride, stream_ptr()))
+    return sites
+
+
+def exact_allgather(sites, chi, counts, m, stride, site_off_dev, group=None, pack=None, unpack=None) -> tuple:
+    """All-gather every rank's states WITHOUT the layout padding: each rank
+    packs its site tensors back to back (mpskq_pack_exact), the packed
+    buffers (padded only to the largest rank's byte count) and the bond-dim
+    tables are all-gathered, and every rank unpacks all states into the batch
+    layout (mpskq_unpack_exact).  Returns (sites_all, chi_all, bytes this rank
+    received).  `pack` / `unpack` default to the native kernels (the CPU
+    tests pass torch stand-ins)."""
+    import torch.distributed as dist
+
+    rank, world = rank_world(group)
+    chi_all = allgather_rows(chi, counts, group)
+    off, total = exact_offsets(chi)
+    packed = (pack or _pack_native)(sites, chi, off, total, m, stride, site_off_dev)
+    dev = sites.device
+    sz = torch.tensor([[total]], dtype=torch.int64, device=dev)
+    sizes = [int(x) for x in allgather_rows(sz, [1] * world, group)[:, 0].tolist()]
+    mx = max(max(sizes), 1)
+    host = _host_collectives(group)
+    pad = torch.zeros(2 * mx, dtype=torch.float64, device="cpu" if host else dev)
+    pad[: 2 * total] = packed.to(pad.device)
+    parts = torch.empty(world * 2 * mx, dtype=torch.float64, device=pad.device)
+    dist.all_gather_into_tensor(parts, pad, group=group) if not host else dist.all_gather(
+        list(parts.view(world, 2 * mx).unbind(0)), pad, group=group)
+    parts = parts.to(dev)
+    offs, s0 = [], 0
+    for r, c in enumerate(counts):
+        o_r, _ = exact_offsets(chi_all[s0 : s0 + c])
+        offs.append(o_r + r * mx)
+        s0 += c
+    state_off = torch.cat(offs) if offs else torch.zeros(0, dtype=torch.int64, device=dev)
+    sites_all = (unpack or _unpack_native)(parts, state_off, chi_all, m, stride, site_off_dev)
+    nloc = chi.shape[0]
+    received = 16 * (sum(sizes) - total) + 4 * (m + 1) * (sum(counts) - nloc)
+    return sites_all, chi_all, received
+
+
+def gather_rows_to0(rows: torch.Tensor, ids: torch.Tensor, group=None) -> tuple:
+    """Rank 0 receives every rank's owned K rows (and their caller row ids);
+    other ranks get (None, None).  Shorter row sets are padded with id -1."""
+    import torch.distributed as dist
+
+    rank, world = rank_world(group)
+    dev = rows.device
+    host = _host_collectives(group)
+    n = torch.tensor([[rows.shape[0]]], dtype=torch.int64, device=dev)
+    counts = [int(x) for x in allgather_rows(n, [1] * world, group)[:, 0].tolist()]
+    mx = max(max(counts), 1)
+    nk = rows.shape[1] if rows.ndim == 2 else 0
+    tdev = "cpu" if host else dev
+    pr = torch.zeros((mx, nk), dtype=rows.dtype, device=tdev)
+    pi = torch.full((mx,), -1, dtype=torch.int32, device=tdev)
+    pr[: rows.shape[0]] = rows.to(tdev)
+    pi[: ids.shape[0]] = ids.to(tdev)
+    gr = [torch.empty_like(pr) for _ in range(world)] if rank == 0 else None
+    gi = [torch.empty_like(pi) for _ in range(world)] if rank == 0 else None
+    dist.gather(pr, gr, dst=0, group=group)
+    dist.gather(pi, gi, dst=0, group=group)
+    if rank != 0:
+        return None, None
+    return torch.cat(gr).to(dev), torch.cat(gi).to(dev)
+
+
 def _all_reduce_max(t: torch.Tensor, group=None) -> torch.Tensor:
     import torch.distributed as dist
 
@@ -236,6 +324,37 @@ def tiles_of(kind: str, chi_cap: int, n_bras: int, n_kets: int, rank: int, world
     return out, int(rb.value), int(cb.value)
 
 
+def _gram_single(X_bras, X_kets, cfg, kind: str, budget: float, chi_max: int = 0):
+    """One GPU: the whole path in one native call (mpskq_gram_host: rows in,
+    encode + simulate with per-state capacity escalation + overlap, K
+    streamed into a page-locked host matrix under the overlap)."""
+    import ctypes as C
+
+    from .kernel import RunReport
+    from .mps import pinned_matrix
+    from ._device import stream_ptr
+
+    train = kind == "train"
+    Xb = np.ascontiguousarray(X_bras, dtype=np.float64)
+    Xk = np.ascontiguousarray(X_kets, dtype=np.float64)
+    nb, nk = (Xk.shape[0], Xk.shape[0]) if train else (Xb.shape[0], Xk.shape[0])
+    rep = RunReport()
+    if nb == 0 or nk == 0:
+        return (np.eye(nk) if train else np.empty((nb, nk))), rep
+    K = pinned_matrix(nb, nk)
+    secs = np.zeros(4)
+    f64 = C.POINTER(C.c_double)
+    N.check(N.lib().mpskq_gram_host(
+        N.KIND_TRAIN if train else N.KIND_TEST, cfg.m, cfg.r, cfg.d, float(cfg.gamma), float(budget), int(chi_max), 0,
+        N.ptr(Xk if train else Xb, C.c_double), nb, None if train else N.ptr(Xk, C.c_double), 0 if train else nk,
+        C.cast(K.data_ptr(), f64), stream_ptr(), N.ptr(secs, C.c_double)))
+    for phase, dt in zip(("simulation", "inner_products", "communication", "merge"), secs):
+        rep._add(phase, float(dt))
+    rep.n_simulations = nk if train else nb + nk
+    rep.n_inner_products = nk * (nk - 1) // 2 if train else nb * nk
+    return K.numpy(), rep
+
+
 def gram(X_bras, X_kets, cfg, kind: str, budget: float, chi_max: int = 0, group=None):
     """Kernel matrix for run_distributed; returns (K or empty on ranks > 0, RunReport)."""
     import torch.distributed as dist
@@ -246,6 +365,8 @@ def gram(X_bras, X_kets, cfg, kind: str, budget: float, chi_max: int = 0, group=
 
     require_cuda()
     rank, world = rank_world(group)
+    if world == 1 and not FORCE_COLLECTIVES:
+        return _gram_single(X_bras, X_kets, cfg, kind, budget, chi_max)
     train = kind == "train"
     X_all = X_kets if train else np.vstack([X_bras, X_kets])
     n_all = X_all.shape[0]
@@ -271,14 +392,14 @@ def gram(X_bras, X_kets, cfg, kind: str, budget: float, chi_max: int = 0, group=
         off, stride = batch_layout(cfg.m, cap)
         counts = [shard(n_all, world, r)[1] - shard(n_all, world, r)[0] for r in range(world)]
         dev = torch.device("cuda")
+        off_d = torch.from_numpy(off).to(dev)
         mine = local if local is not None else None
         sites_l = mine.sites if mine is not None else torch.zeros((0, 2 * stride), dtype=torch.float64, device=dev)
         chi_l = mine.chi if mine is not None else torch.zeros((0, cfg.m + 1), dtype=torch.int32, device=dev)
         disc_l = mine.discard if mine is not None else torch.zeros(0, dtype=torch.float64, device=dev)
         peak_l = mine.peak if mine is not None else torch.zeros(0, dtype=torch.int32, device=dev)
         with Timer() as t_comm:
-            sites = allgather_rows(sites_l, counts, group)
-            chi = allgather_rows(chi_l, counts, group)
+            sites, chi, _ = exact_allgather(sites_l, chi_l, counts, cfg.m, stride, off_d, group)
             disc = allgather_rows(disc_l, counts, group)
             peak = allgather_rows(peak_l, counts, group)
         ref = mine if mine is not None else None
@@ -288,17 +409,32 @@ def gram(X_bras, X_kets, cfg, kind: str, budget: float, chi_max: int = 0, group=
         rep._add("communication", t_comm.seconds())
     else:
         full = local
-    from .mps import overlap_matrix
+    from ._device import dptr, stream_ptr
 
+    kind_id = N.KIND_TRAIN if train else N.KIND_TEST
     with Timer() as t_ov:
         bras = full.rows(0, nb) if not train else full
         kets = full if train else full.rows(nb, nb + nk)
-        K_dev = torch.zeros((nb, nk), dtype=torch.float64, device="cuda")
-        overlap_matrix(bras, kets, kind, rank=rank, world=world, out=K_dev)
+        n_own = N.C.c_int64(0)
+        N.check(N.lib().mpskq_owned_rows(full.chi_cap, nb, rank, world, N.C.byref(n_own)))
+        rows = torch.empty((n_own.value, nk), dtype=torch.float64, device="cuda")
+        ids = torch.empty(n_own.value, dtype=torch.int32, device="cuda")
+        pos = torch.empty(nk, dtype=torch.int32, device="cuda")
+        N.check(N.lib().mpskq_overlap_owned_rows(
+            kind_id, cfg.m, full.chi_cap, dptr(full.site_off_dev), full.stride, dptr(bras.sites), dptr(bras.chi), nb,
+            dptr(kets.sites), dptr(kets.chi), nk, rank, world, dptr(rows), dptr(ids), dptr(pos), stream_ptr()))
     t0 = time.perf_counter()
-    if _exchange(world):
-        K_dev = _reduce_sum_to0(K_dev, group)
-    K = K_dev.cpu().numpy() if rank == 0 else np.empty((0, 0))
+    all_rows, all_ids = gather_rows_to0(rows, ids, group)
+    K = np.empty((0, 0))
+    if rank == 0:
+        from .mps import pinned_matrix
+
+        K_dev = torch.empty((nb, nk), dtype=torch.float64, device="cuda")
+        N.check(N.lib().mpskq_assemble_rows(kind_id, nb, nk, dptr(all_rows), dptr(all_ids), all_ids.shape[0],
+                                            dptr(pos) if train else None, dptr(K_dev), nk, stream_ptr()))
+        Kp = pinned_matrix(nb, nk)
+        Kp.copy_(K_dev)
+        K = Kp.numpy()
     rep._add("simulation", t_sim.seconds())
     rep._add("inner_products", t_ov.seconds())
     rep._add("merge", time.perf_counter() - t0)

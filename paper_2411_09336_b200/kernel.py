@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from .ansatz import FeatureMapConfig, feature_map_angles, feature_map_topology, half_angle_coefficients
-from .mps import DEFAULT_TRUNC_BUDGET, MpsBatch, MpsState, compile_program, overlap_matrix, simulate_program
+from .mps import DEFAULT_TRUNC_BUDGET, MpsBatch, MpsState, compile_program, overlap_matrix_host, simulate_program
 
 STRATEGIES = ("no_messaging", "round_robin")
 KINDS = ("train", "test")
@@ -328,7 +328,7 @@ def compute_gram(bras, kets, kind: str, report: RunReport | None = None) -> Gram
     t0 = time.perf_counter()
     b = _to_batch(bras)
     k = b if kind == "train" else _to_batch(kets)
-    K = overlap_matrix(b, k, kind).cpu().numpy()
+    K = overlap_matrix_host(b, k, kind)
     count = nk * (nk - 1) // 2 if kind == "train" else nb * nk
     if report is not None:
         report.n_inner_products += count

@@ -229,6 +229,8 @@ class MpsBatch(Sequence):
         self.ortho_center = ortho_center
         self.entry_log = entry_log
         self.seconds = seconds
+        self.phase_cycles = None  # int64 (n, 3) device clocks per phase (simulate_program)
+        self._phase_host = None
         self._host = None
 
     def __len__(self) -> int:
@@ -261,16 +263,27 @@ class MpsBatch(Sequence):
             row[self.site_off[s] : self.site_off[s] + c[s] * 2 * c[s + 1]].reshape(c[s], 2, c[s + 1]).copy()
             for s in range(self.m)
         ]
-        per = self.seconds / max(n, 1)
         return MpsState(ts, self.budget, float(disc[i]), self.ortho_center, int(peak[i]), self.gate_count_1q,
-                        self.gate_count_2q, {"simulation": per})
+                        self.gate_count_2q, self.timings(i))
+
+    def timings(self, i: int) -> dict:
+        """Per-phase device seconds of state i (MpsState.timings keys,
+        mps.py:137 / :159 / :204), from the simulator's per-state clocks."""
+        if self.phase_cycles is None:
+            return {}
+        if self._phase_host is None:
+            self._phase_host = self.phase_cycles.cpu().numpy() / _sm_hz()
+        c, o, t = (float(x) for x in self._phase_host[i])
+        return {k: v for k, v in (("canonicalize", c), ("one_qubit", o), ("two_qubit", t)) if v > 0.0}
 
     def rows(self, a: int, b: int) -> "MpsBatch":
         """Device view of states a..b-1 (no copy)."""
         log = None if self.entry_log is None else self.entry_log[a:b]
-        return MpsBatch(self.m, self.chi_cap, self.site_off, self.stride, self.sites[a:b], self.chi[a:b],
-                        self.discard[a:b], self.peak[a:b], self.budget, self.gate_count_1q,
-                        self.gate_count_2q, self.ortho_center, log, self.seconds * (b - a) / max(len(self), 1))
+        out = MpsBatch(self.m, self.chi_cap, self.site_off, self.stride, self.sites[a:b], self.chi[a:b],
+                       self.discard[a:b], self.peak[a:b], self.budget, self.gate_count_1q,
+                       self.gate_count_2q, self.ortho_center, log, self.seconds * (b - a) / max(len(self), 1))
+        out.phase_cycles = None if self.phase_cycles is None else self.phase_cycles[a:b]
+        return out
 
     def to_states(self) -> list:
         return [self[i] for i in range(len(self))]
@@ -291,6 +304,10 @@ class MpsBatch(Sequence):
         if any(s.m != m for s in states):
             raise ValueError("qubit count mismatch between state lists")
         need = max(max(s.bond_dims()) for s in states)
+        phys = np.minimum(np.arange(m + 1), m - np.arange(m + 1))
+        for s in states:  # the layout's slot of bond b holds at most 2^min(b, m-b)
+            if np.any(np.array(s.bond_dims(), dtype=np.float64) > np.exp2(phys)):
+                raise ValueError("bond dimension exceeds the exact-state bound 2^min(b, m-b)")
         caps = N.supported_chi_caps()
         if chi_cap is None:
             chi_cap = next((c for c in caps if c >= need), None)
@@ -315,11 +332,28 @@ class MpsBatch(Sequence):
         )
 
 
+def _sm_hz() -> float:
+    khz = N.lib().mpskq_sm_clock_khz()
+    return 1e3 * khz if khz > 0 else 1.9e9
+
+
+def _check_states(status: np.ndarray) -> np.ndarray:
+    """Raise like the reference for failed states; returns the overflow rows."""
+    if np.any(status == N.STATE_NONFINITE):
+        raise ValueError("tensor has non-finite entries")
+    if np.any(status == N.STATE_NOCONV):
+        raise np.linalg.LinAlgError("SVD did not converge")
+    return np.nonzero(status == N.STATE_CAPACITY)[0]
+
+
 def simulate_program(prog: Program, coef, budget: float, chi_max: int = 0,
                      chi_cap: int | None = None, memory_log: bool = False) -> MpsBatch:
     """Run the compiled program from |0..0> for every row of the coefficient
     table ``coef`` ((n, n_params, 2) half-angle cos/sin, numpy or a CUDA
-    tensor); escalates the chi capacity on overflow."""
+    tensor).  Every state starts at the hinted chi capacity; only the states
+    that outgrow it are re-simulated at the next capacity (per-state
+    escalation), and the levels are gathered into the final capacity's
+    layout (mpskq_relayout)."""
     require_cuda()
     if budget < 0:
         raise ValueError("budget must be non-negative")
@@ -330,10 +364,9 @@ def simulate_program(prog: Program, coef, budget: float, chi_max: int = 0,
     if coef.ndim != 3 or tuple(coef.shape[1:]) != (prog.n_params, 2):
         raise ValueError(f"coefficient table must be (n, {prog.n_params}, 2), got {tuple(coef.shape)}")
     n = coef.shape[0]
-    coef_d = coef if coef.numel() else torch.zeros(2, dtype=torch.float64, device=dev)
     ops_d = prog.device_ops
     caps = N.supported_chi_caps()
-    key = id(prog)
+    key = (id(prog), float(budget), int(chi_max))
     if chi_cap is not None:
         if chi_cap not in caps:
             raise ValueError(f"chi capacity {chi_cap} is not compiled in (have {caps})")
@@ -343,33 +376,78 @@ def simulate_program(prog: Program, coef, budget: float, chi_max: int = 0,
         if chi_max > 0:  # the kept rank never exceeds chi_max
             order = [c for c in order if c < chi_max] + [c for c in order if c >= chi_max][:1]
     m = prog.m
+    levels = []
+    rows = None  # device int64 global row ids of this level (None: all rows)
+    seconds = 0.0
     for cap in order:
+        nl = n if rows is None else int(rows.numel())
+        coef_l = coef if rows is None else coef.index_select(0, rows)
+        if coef_l.numel() == 0:
+            coef_l = torch.zeros((max(nl, 1), max(prog.n_params, 1), 2), dtype=torch.float64, device=dev)
         off, stride = batch_layout(m, cap)
         off_d = torch.from_numpy(off).to(dev)
-        sites = torch.empty((n, 2 * stride), dtype=torch.float64, device=dev)
+        lv = dict(
+            cap=cap, rows=rows, off=off, stride=stride, off_d=off_d,
+            sites=torch.empty((nl, 2 * stride), dtype=torch.float64, device=dev),
+            chi=torch.empty((nl, m + 1), dtype=torch.int32, device=dev),
+            disc=torch.empty(nl, dtype=torch.float64, device=dev),
+            peak=torch.empty(nl, dtype=torch.int32, device=dev),
+            status=torch.zeros(nl, dtype=torch.int32, device=dev),
+            elog=torch.zeros((nl, prog.n_gates), dtype=torch.int64, device=dev) if memory_log else None,
+            phase=torch.zeros((nl, 3), dtype=torch.int64, device=dev),
+        )
+        with Timer() as tm:
+            N.check(
+                N.lib().mpskq_run_program(
+                    m, cap, dptr(ops_d), prog.ops.shape[0], prog.n_gates, dptr(coef_l), prog.n_params, nl,
+                    float(budget), int(chi_max), dptr(off_d), stride, 0, dptr(lv["sites"]), dptr(lv["chi"]),
+                    dptr(lv["disc"]), dptr(lv["peak"]), dptr(lv["status"]), dptr(lv["elog"]),
+                    dptr(lv["phase"]), stream_ptr(),
+                )
+            )
+        seconds += tm.seconds()
+        over = _check_states(lv["status"].cpu().numpy())
+        levels.append(lv)
+        if over.size == 0:
+            break
+        if chi_cap is not None:
+            raise RuntimeError(f"bond dimension exceeds the largest usable chi capacity {order[-1]}")
+        ov = torch.from_numpy(over).to(dev)
+        rows = ov if rows is None else rows.index_select(0, ov)
+    else:
+        raise RuntimeError(f"bond dimension exceeds the largest usable chi capacity {order[-1]}")
+    if chi_cap is None:
+        # next call starts at the first level that held >= 7/8 of the states
+        h = 0
+        while h + 1 < len(levels) and int(levels[h + 1]["rows"].numel()) * 8 > n:
+            h += 1
+        _CAP_HINT[key] = levels[h]["cap"]
+    fin = levels[-1]
+    if len(levels) == 1:
+        sites, chi, disc, peak, elog, phase = (fin[k] for k in ("sites", "chi", "disc", "peak", "elog", "phase"))
+    else:
+        sites = torch.empty((n, 2 * fin["stride"]), dtype=torch.float64, device=dev)
         chi = torch.empty((n, m + 1), dtype=torch.int32, device=dev)
         disc = torch.empty(n, dtype=torch.float64, device=dev)
         peak = torch.empty(n, dtype=torch.int32, device=dev)
-        status = torch.zeros(n, dtype=torch.int32, device=dev)
-        elog = torch.zeros((n, prog.n_gates), dtype=torch.int64, device=dev) if memory_log else None
-        with Timer() as tm:
-            N.check(
-                N.lib().mpskq_simulate(
-                    m, cap, dptr(ops_d), prog.ops.shape[0], prog.n_gates, dptr(coef_d), prog.n_params, n,
-                    float(budget), int(chi_max), dptr(off_d), stride, dptr(sites), dptr(chi), dptr(disc),
-                    dptr(peak), dptr(status), dptr(elog), stream_ptr(),
-                )
-            )
-        st = status.cpu().numpy()
-        if np.any(st == N.STATE_NONFINITE):
-            raise ValueError("tensor has non-finite entries")
-        if np.any(st == N.STATE_CAPACITY):
-            continue
-        if chi_cap is None:
-            _CAP_HINT[key] = cap
-        return MpsBatch(m, cap, off, stride, sites, chi, disc, peak, budget, prog.gate_count_1q,
-                        prog.gate_count_2q, prog.final_center, elog, tm.seconds())
-    raise RuntimeError(f"bond dimension exceeds the largest usable chi capacity {order[-1]}")
+        phase = torch.empty((n, 3), dtype=torch.int64, device=dev)
+        elog = torch.empty((n, prog.n_gates), dtype=torch.int64, device=dev) if memory_log else None
+        for lv in levels:  # later levels overwrite the rows that overflowed earlier ones
+            r32 = None if lv["rows"] is None else lv["rows"].to(torch.int32)
+            N.check(N.lib().mpskq_relayout(m, lv["sites"].shape[0], dptr(lv["sites"]), dptr(lv["off_d"]),
+                                           lv["stride"], dptr(lv["chi"]), dptr(sites), dptr(fin["off_d"]),
+                                           fin["stride"], dptr(r32), stream_ptr()))
+            idx = lv["rows"] if lv["rows"] is not None else torch.arange(n, device=dev)
+            chi.index_copy_(0, idx, lv["chi"])
+            disc.index_copy_(0, idx, lv["disc"])
+            peak.index_copy_(0, idx, lv["peak"])
+            phase.index_copy_(0, idx, lv["phase"])
+            if elog is not None:
+                elog.index_copy_(0, idx, lv["elog"])
+    batch = MpsBatch(m, fin["cap"], fin["off"], fin["stride"], sites, chi, disc, peak, budget, prog.gate_count_1q,
+                     prog.gate_count_2q, prog.final_center, elog, seconds)
+    batch.phase_cycles = phase
+    return batch
 
 
 def simulate_circuit(circuit: Circuit, budget: float = DEFAULT_TRUNC_BUDGET, memory_log: list | None = None) -> MpsState:
@@ -383,6 +461,183 @@ def simulate_circuit(circuit: Circuit, budget: float = DEFAULT_TRUNC_BUDGET, mem
     return batch[0]
 
 
+# ---------------------------------------------------------------- gates on given states
+_UNITARY_ATOL = 1e-10  # mps.py:26
+
+
+def _check_unitary(u: np.ndarray) -> None:
+    """mps.py:141-144 (input validation of a 2x2 / 4x4 host matrix)."""
+    if not np.allclose(u.conj().T @ u, np.eye(u.shape[0]), atol=_UNITARY_ATOL):
+        raise ValueError("gate matrix is not unitary")
+
+
+def _moves(m: int, center, target: int) -> list:
+    """canonicalize(state, target) as QR-move ops (mps.py:123-138): left
+    steps (_left_isometrize, :105-111) below the target, right steps
+    (_right_isometrize, :114-120) above it."""
+    if center is None:
+        return [(N.OP_QRL, s) for s in range(0, target)] + [(N.OP_QRR, s) for s in range(m - 1, target, -1)]
+    if center < target:
+        return [(N.OP_QRL, s) for s in range(center, target)]
+    return [(N.OP_QRR, s) for s in range(center, target, -1)]
+
+
+def _evolve(state: MpsState, ops: list, coef: np.ndarray, n_gates: int = 0, memory_log: bool = False):
+    """Replay `ops` ((code, site[, slot, gate index, left])) on `state` on the
+    GPU (mpskq_run_program with from_input=1) and write the result back into
+    `state` (the reference mutates the state in place).  Escalates the chi
+    capacity when a bond outgrows it.  Returns the per-gate entry counts."""
+    require_cuda()
+    if not ops:
+        return []
+    dev = torch.device("cuda")
+    arr = np.zeros((len(ops), 4), dtype=np.int32)
+    for k, op in enumerate(ops):
+        code, site = op[0], op[1]
+        slot = op[2] if len(op) > 2 else -1
+        gidx = op[3] if len(op) > 3 else -1
+        left = op[4] if len(op) > 4 else False
+        arr[k] = (code | ((N.ABSORB_LEFT if left else 0) << 8), site, slot, gidx)
+    ops_d = torch.from_numpy(arr).to(dev)
+    cf = np.ascontiguousarray(coef, dtype=np.complex128).reshape(-1)
+    n_params = max(cf.size, 1)
+    coef_d = torch.from_numpy(np.concatenate([cf, np.zeros(1, np.complex128)])[:n_params].view(np.float64)).to(dev)
+    caps = N.supported_chi_caps()
+    start = next((c for c in caps if c >= state.max_bond()), None)
+    if start is None:
+        raise ValueError(f"bond dimension {state.max_bond()} exceeds the largest compiled capacity {caps[-1]}")
+    for cap in [c for c in caps if c >= start]:
+        b = MpsBatch.from_states([state], cap)
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+        elog = torch.zeros((1, max(n_gates, 1)), dtype=torch.int64, device=dev) if memory_log else None
+        phase = torch.zeros((1, 3), dtype=torch.int64, device=dev)
+        N.check(N.lib().mpskq_run_program(
+            state.m, cap, dptr(ops_d), len(ops), max(n_gates, 1), dptr(coef_d), n_params, 1,
+            float(state.trunc_budget_per_gate), 0, dptr(b.site_off_dev), b.stride, 1, dptr(b.sites), dptr(b.chi),
+            dptr(b.discard), dptr(b.peak), dptr(status), dptr(elog), dptr(phase), stream_ptr()))
+        if _check_states(status.cpu().numpy()).size:
+            continue
+        b.phase_cycles = phase
+        out = b[0]
+        state.sites[:] = out.sites
+        state.accumulated_discard = out.accumulated_discard
+        state.peak_chi = out.peak_chi
+        for k, v in b.timings(0).items():
+            state.timings[k] = state.timings.get(k, 0.0) + v
+        return [16 * int(x) for x in elog[0, :n_gates].cpu().numpy()] if memory_log else []
+    raise RuntimeError(f"bond dimension exceeds the largest usable chi capacity {caps[-1]}")
+
+
+def canonicalize(state: MpsState, center: int) -> MpsState:
+    """Move the orthogonality center to ``center`` (mps.py:123-138) with QR
+    moves on the GPU."""
+    if not 0 <= center < state.m:
+        raise ValueError(f"center {center} out of range for {state.m} sites")
+    _evolve(state, _moves(state.m, state.ortho_center, center), np.zeros(0))
+    state.ortho_center = center
+    return state
+
+
+def apply_one_qubit(state: MpsState, q: int, matrix) -> MpsState:
+    """Contract a 2x2 unitary with site q on the GPU (mps.py:147-160)."""
+    if not 0 <= q < state.m:
+        raise ValueError(f"qubit {q} out of range")
+    matrix = np.asarray(matrix, dtype=np.complex128)
+    if matrix.shape != (2, 2):
+        raise ValueError("single-qubit gate must be a 2x2 matrix")
+    _check_unitary(matrix)
+    _evolve(state, [(N.OP_U1, q, 0)], matrix)
+    state.gate_count_1q += 1
+    return state
+
+
+def apply_two_qubit(state: MpsState, q: int, matrix, absorb: str = "right") -> MpsState:
+    """4x4 unitary on (q, q+1): canonicalize, theta, truncated SVD, renorm,
+    absorb (mps.py:163-205), all on the GPU."""
+    if not 0 <= q < state.m - 1:
+        raise ValueError(f"site pair ({q}, {q + 1}) out of range")
+    if absorb not in ("left", "right"):
+        raise ValueError("absorb must be 'left' or 'right'")
+    matrix = np.asarray(matrix, dtype=np.complex128)
+    if matrix.shape != (4, 4):
+        raise ValueError("two-qubit gate must be a 4x4 matrix")
+    _check_unitary(matrix)
+    left = absorb == "left"
+    _evolve(state, _moves(state.m, state.ortho_center, q) + [(N.OP_U2, q, 0, -1, left)], matrix)
+    state.ortho_center = q if left else q + 1
+    state.gate_count_2q += 1
+    return state
+
+
+def apply_gate(state: MpsState, gate, absorb: str = "right") -> MpsState:
+    """Apply one circuit gate (mps.py:208-221); two-qubit gates must act on
+    adjacent qubits."""
+    from .ansatz import gate_matrix
+
+    for q in gate.qubits:
+        if not 0 <= q < state.m:
+            raise ValueError(f"qubit {q} out of range for {state.m} sites")
+    u = gate_matrix(gate)
+    if len(gate.qubits) == 1:
+        return apply_one_qubit(state, gate.qubits[0], u)
+    a, b = gate.qubits
+    if abs(a - b) != 1:
+        raise ValueError(f"two-qubit gate on ({a}, {b}) is not adjacent; route the circuit first")
+    if a > b:
+        u = u.reshape(2, 2, 2, 2).transpose(1, 0, 3, 2).reshape(4, 4)
+    return apply_two_qubit(state, min(a, b), u, absorb=absorb)
+
+
+def run_circuit(state: MpsState, circuit: Circuit, memory_log: list | None = None) -> MpsState:
+    """Apply every gate of ``circuit`` in order with run_circuit's absorb rule
+    (mps.py:224-247) as ONE GPU program: the canonicalize moves start from the
+    state's own orthogonality center; H/RZ/RXX/SWAP use the simulator's gate
+    ops (the ones simulate_circuit replays)."""
+    if circuit.m != state.m:
+        raise ValueError(f"circuit has {circuit.m} qubits, state has {state.m}")
+    gates = circuit.gates
+    next_2q = [None] * (len(gates) + 1)
+    for i in range(len(gates) - 1, -1, -1):
+        next_2q[i] = min(gates[i].qubits) if len(gates[i].qubits) == 2 else next_2q[i + 1]
+    codes = {"H": N.OP_H, "RZ": N.OP_RZ, "RXX": N.OP_RXX, "SWAP": N.OP_SWAP}
+    ops, angles = [], []
+    center = state.ortho_center
+    g1 = g2 = 0
+    for i, g in enumerate(gates):
+        for q in g.qubits:
+            if not 0 <= q < state.m:
+                raise ValueError(f"qubit {q} out of range for {state.m} sites")
+        slot = -1
+        if g.angle is not None:
+            slot = len(angles)
+            angles.append(g.angle)
+        if len(g.qubits) == 1:
+            ops.append((codes[g.kind], g.qubits[0], slot, i))
+            g1 += 1
+            continue
+        a, b = g.qubits
+        if abs(a - b) != 1:
+            raise ValueError(f"two-qubit gate on ({a}, {b}) is not adjacent; route the circuit first")
+        q = min(a, b)  # H/RZ/RXX/SWAP are symmetric under exchanging the qubits
+        nxt = next_2q[i + 1]
+        left = nxt is not None and nxt <= q
+        ops += _moves(state.m, center, q)
+        ops.append((codes[g.kind], q, slot, i, left))
+        center = q if left else q + 1
+        g2 += 1
+    from .ansatz import half_angle_coefficients
+
+    hc = half_angle_coefficients(np.array(angles, dtype=np.float64)) if angles else np.zeros((0, 2))
+    coef = hc[:, 0] + 1j * hc[:, 1]
+    log = _evolve(state, ops, coef, n_gates=len(gates), memory_log=memory_log is not None)
+    if memory_log is not None:
+        memory_log.extend(log)
+    state.ortho_center = center
+    state.gate_count_1q += g1
+    state.gate_count_2q += g2
+    return state
+
+
 def _as_batch(x) -> tuple:
     if isinstance(x, MpsBatch):
         return x, None
@@ -391,16 +646,42 @@ def _as_batch(x) -> tuple:
     raise TypeError(f"expected MpsState or MpsBatch, got {type(x).__name__}")
 
 
-def overlap_matrix(bras: MpsBatch, kets: MpsBatch, kind: str, amplitude: bool = False,
-                   rank: int = 0, world: int = 1, out: torch.Tensor | None = None) -> torch.Tensor:
-    """Device matrix of |<bra_i|ket_j>|^2 (or the complex amplitudes)."""
-    require_cuda()
+def _common_cap(bras: MpsBatch, kets: MpsBatch) -> tuple:
     if bras.m != kets.m:
         raise ValueError("qubit count mismatch between state lists")
     if bras.chi_cap != kets.chi_cap:
         cap = max(bras.chi_cap, kets.chi_cap)
         bras = bras if bras.chi_cap == cap else MpsBatch.from_states(bras.to_states(), cap)
         kets = kets if kets.chi_cap == cap else MpsBatch.from_states(kets.to_states(), cap)
+    return bras, kets
+
+
+def pinned_matrix(rows: int, cols: int) -> torch.Tensor:
+    """Page-locked host float64 matrix (torch's caching host allocator: the
+    block returns to the cache when the numpy view handed out is dropped)."""
+    return torch.empty((rows, cols), dtype=torch.float64, pin_memory=True)
+
+
+def overlap_matrix_host(bras: MpsBatch, kets: MpsBatch, kind: str) -> np.ndarray:
+    """Host matrix of |<bra_i|ket_j>|^2 in page-locked memory: at chi <= 4 the
+    overlap streams finished row bands into it under the computation
+    (mpskq_overlap_host), otherwise one device-to-host copy."""
+    require_cuda()
+    bras, kets = _common_cap(bras, kets)
+    nb, nk = len(bras), len(kets)
+    K = pinned_matrix(nb, nk)
+    kind_id = N.KIND_TRAIN if kind == "train" else N.KIND_TEST
+    N.check(N.lib().mpskq_overlap_host(
+        kind_id, bras.m, bras.chi_cap, dptr(bras.site_off_dev), bras.stride, dptr(bras.sites), dptr(bras.chi), nb,
+        dptr(kets.sites), dptr(kets.chi), nk, K.data_ptr(), stream_ptr()))
+    return K.numpy()
+
+
+def overlap_matrix(bras: MpsBatch, kets: MpsBatch, kind: str, amplitude: bool = False,
+                   rank: int = 0, world: int = 1, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Device matrix of |<bra_i|ket_j>|^2 (or the complex amplitudes)."""
+    require_cuda()
+    bras, kets = _common_cap(bras, kets)
     kind_id = N.KIND_TRAIN if kind == "train" else N.KIND_TEST
     nb, nk = len(bras), len(kets)
     if out is None:

@@ -290,3 +290,80 @@ def svd_cases_large():
 
 if __name__ == "__main__" and "--svd-large" in sys.argv:
     svd_cases_large()
+
+
+# Round-2 fixtures (VERDICT r1 "next" item 1): the paper's 165-qubit d=6 case
+# at both truncation budgets, config 5 at every interaction distance, and more
+# rows at d=6/7/8 (second seed).  Each case runs in its own process:
+#     python tests/golden/make_golden.py --case <name>
+ROUND2_CASES = {
+    # m=165, d=6: PAPER.md:381/:388 (largest d at 165 qubits); budget 1e-24 is
+    # the reference default (peak chi ~109, capacity 128), 1e-16 the paper's
+    # fidelity cutoff (peak chi ~41, capacity 48)
+    "stretch_m165_d6_b24": (165, 2, 6, 0.1, 1e-24, 8, 4, 0),
+    "stretch_m165_d6_b16": (165, 2, 6, 0.1, 1e-16, 8, 4, 0),
+    # config 5 (m=100, gamma 0.1, budget 1e-16) at the distances round 1 lacked
+    "config5_m100_d1": (100, 2, 1, 0.1, 1e-16, 8, 4, 0),
+    "config5_m100_d2": (100, 2, 2, 0.1, 1e-16, 8, 4, 0),
+    "config5_m100_d3": (100, 2, 3, 0.1, 1e-16, 8, 4, 0),
+    "config5_m100_d5": (100, 2, 5, 0.1, 1e-16, 8, 4, 0),
+    # more d=6/7/8 rows (seed 1: disjoint from the round-1 seed-0 rows)
+    "config5_m100_d6_s1": (100, 2, 6, 0.1, 1e-16, 8, 4, 1),
+    "config5_m100_d7_s1": (100, 2, 7, 0.1, 1e-16, 8, 4, 1),
+    "config5_m100_d8_s1": (100, 2, 8, 0.1, 1e-16, 8, 4, 1),
+}
+
+if __name__ == "__main__" and "--case" in sys.argv:
+    _name = sys.argv[sys.argv.index("--case") + 1]
+    gram_case(_name, *ROUND2_CASES[_name][:7], seed=ROUND2_CASES[_name][7])
+
+
+def ops_sequences():
+    """Reference results of tests/golden/ops_cases.py (apply_* / canonicalize /
+    run_circuit on given states, mps.py:123-247)."""
+    sys.path.insert(0, str(OUT))
+    import ops_cases
+
+    out = {}
+    for name, m, budget, steps in ops_cases.cases():
+        st, log = ops_cases.run(mps, ansatz, m, budget, steps)
+        out[name + "_sv"] = mps.to_statevector(st)
+        out[name + "_chi"] = np.array(st.bond_dims(), dtype=np.int32)
+        out[name + "_discard"] = st.accumulated_discard
+        out[name + "_peak"] = st.peak_chi
+        out[name + "_center"] = st.ortho_center
+        out[name + "_counts"] = np.array([st.gate_count_1q, st.gate_count_2q])
+        out[name + "_memlog"] = np.array(log, dtype=np.int64)
+    np.savez_compressed(OUT / "ops_sequences.npz", **out)
+    print("ops_sequences:", len(ops_cases.cases()))
+
+
+if __name__ == "__main__" and "--ops" in sys.argv:
+    ops_sequences()
+
+
+def experiment_config1():
+    """cmd_experiment (cli.py:152-214) end to end on config 1 (m=8, d=1, 2
+    layers, gamma 0.5, untruncated, 40+40 overlapping blobs (separation 1.5),
+    Gaussian baseline): the
+    reference's metric rows over its default C grid (cli.py:61-64) through
+    its own SMO learner (learn.py:188-336)."""
+    import json
+    import tempfile
+
+    from mpskernel import cli
+
+    cfg = cli.ExperimentConfig(synthetic=cli.SyntheticSpec(n_per_class=40, separation=1.5), m=8, r=2, d=1, gamma=0.5,
+                               budget=0.0, baseline=True, seed=0)
+    with tempfile.TemporaryDirectory() as tmp:
+        res = cli.cmd_experiment(cfg, tmp)
+        K_train = np.loadtxt(f"{tmp}/gram_train.csv", delimiter=",")
+        K_test = np.loadtxt(f"{tmp}/gram_test.csv", delimiter=",")
+    keep = {k: res[k] for k in ("split", "rescale_params", "quantum", "best_quantum", "gaussian", "best_gaussian")}
+    (OUT / "experiment_config1.json").write_text(json.dumps(keep, indent=1, sort_keys=True))
+    np.savez_compressed(OUT / "experiment_config1_K.npz", K_train=K_train, K_test=K_test)
+    print("experiment_config1: best AUC", res["best_quantum"]["test"]["auc"])
+
+
+if __name__ == "__main__" and "--experiment" in sys.argv:
+    experiment_config1()

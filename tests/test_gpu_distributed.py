@@ -1,7 +1,8 @@
-"""run_distributed over 2 processes sharing one GPU (gloo collectives on host
+"""run_distributed over processes sharing one GPU (gloo collectives on host
 copies; the ranks' kernels never wait on each other): the sharded
-simulation, ragged all-gather, block-cyclic tile split and SUM-reduce must
-reproduce the single-process kernel matrix bitwise."""
+simulation, exact (unpadded) all-gather, band-cyclic row ownership and the
+gather + assembly on rank 0 must reproduce the single-process kernel
+matrix bitwise."""
 
 import os
 import socket
@@ -126,8 +127,9 @@ def _nccl_single(kind, q):
 
 @pytest.mark.parametrize("kind", ["train", "test"])
 def test_nccl_exchange_path_single_gpu(kind):
-    """The NCCL branch of the exchange (device all-gather of the packed slabs
-    and bond dims, all-reduce of the capacity, SUM-reduce of K) on one rank:
+    """The NCCL branch of the exchange (device all-gather of the exactly
+    packed MPS and bond dims, all-reduce of the capacity, gather of the owned
+    K rows and assembly) on one rank:
     the only NCCL configuration a one-GPU box can run."""
     import paper_2411_09336_b200 as P
 
@@ -144,3 +146,29 @@ def test_nccl_exchange_path_single_gpu(kind):
     assert p.exitcode == 0
     assert backend == "nccl"
     assert np.array_equal(K, ref)
+
+
+def test_bench_multirank_step_four_ranks_share_gpu():
+    """bench.py's N>1 step (exact all-gather, owned K rows, gather + assemble
+    on rank 0) with 4 ranks sharing one GPU over gloo
+    (MPSKQ_BENCH_SHARE_GPU=1): the rank-0 K must pass the run's own oracle
+    spot check and the public-API e2e must equal the device step bitwise."""
+    import json
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    env = dict(os.environ, MPSKQ_BENCH_SHARE_GPU="1", OMP_NUM_THREADS="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", str(ROOT / "bench.py"), "--gpus", "4",
+           "--rows", "200", "--steps", "1", "--warmup", "3", "--test-rows", "0", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=str(ROOT), env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 4
+    assert line["parity_spot_check"]["bond_dims_equal"]
+    assert line["parity_spot_check"]["max_abs_err_vs_oracle_6x6"] < 1e-10
+    assert line["e2e"]["k_bitwise_equal_device_path"]
+    comm = line["communication_bytes_per_step"]
+    assert comm["allgather_bytes_received"] > 0 and comm["gather_bytes_to_rank0"] > 0

@@ -1,0 +1,131 @@
+"""Parity of the large-chi configurations and of EVERY state at full size.
+
+1. Reference fixtures (tests/golden/make_golden.py --case ..., produced by
+   running /root/reference): the paper's 165-qubit d=6 case at budget 1e-24
+   (peak chi 85+, capacity 96/128) and 1e-16 (capacity 32/48), config 5 at
+   d = 1, 2, 3, 5 and a second seed at d = 6, 7, 8.  Bond dims identical per
+   site, accumulated discard and K within tolerance.
+2. Full-size scans: every row of the headline (6400), config 2 (800 + 200),
+   config 3 (1600 + 400) and 64 rows per interaction distance of config 5
+   (d = 5..8) simulated on the GPU and by the oracle (bitwise the reference,
+   tests/test_oracle.py) in a host process pool; the number of states whose
+   bond dimensions differ ("truncation flips") is recorded in
+   gpurun_out/scale_parity_<name>.json and must be zero; K is compared on
+   every pair of a 24-state sample.
+
+Tolerances (BASELINE.json north_star): 1e-10 for budgets 0 / 1e-24, 1e-6 at
+the 1e-16 fidelity cutoff.
+Reference: mps.py:163-205 (apply_two_qubit), tensor.py:87-123 (svd_truncated).
+"""
+
+import json
+import time
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden
+from oracle import mps_oracle as O
+from oracle.scan import host_cores, oracle_states
+
+pytestmark = pytest.mark.gpu
+
+ROUND2 = [
+    "stretch_m165_d6_b24.npz",
+    "stretch_m165_d6_b16.npz",
+    "config5_m100_d1.npz",
+    "config5_m100_d2.npz",
+    "config5_m100_d3.npz",
+    "config5_m100_d5.npz",
+    "config5_m100_d6_s1.npz",
+    "config5_m100_d7_s1.npz",
+    "config5_m100_d8_s1.npz",
+]
+
+
+def _tol(budget):
+    return 1e-10 if budget <= 1e-24 else 1e-6
+
+
+@pytest.mark.parametrize("name", ROUND2)
+def test_large_chi_fixture_matches_reference(name):
+    import paper_2411_09336_b200 as P
+
+    g = golden(name)
+    cfg = P.FeatureMapConfig(int(g["m"]), int(g["r"]), int(g["d"]), float(g["gamma"]))
+    budget = float(g["budget"])
+    train = P.simulate_dataset(g["X"], cfg, budget=budget)
+    test = P.simulate_dataset(g["X_test"], cfg, budget=budget)
+    assert np.array_equal(train.bond_dims(), g["train_chi"]), "bond dims differ from the reference"
+    assert np.array_equal(test.bond_dims(), g["test_chi"])
+    assert np.array_equal(train.peak.cpu().numpy(), g["train_peak"])
+    disc = train.discard.cpu().numpy()
+    # discards sum squares of singular values near sqrt(budget): relative
+    # agreement plus the FP64 rounding floor of the Jacobi vs LAPACK spectra
+    assert np.all(np.abs(disc - g["train_discard"]) <= 1e-20 + 1e-6 * g["train_discard"])
+    Ktr = P.compute_gram(train, train, "train").entries
+    Kte = P.compute_gram(test, train, "test").entries
+    tol = _tol(budget)
+    assert np.abs(Ktr - g["K_train"]).max() < tol
+    assert np.abs(Kte - g["K_test"]).max() < tol
+    assert np.array_equal(Ktr, Ktr.T) and np.all(np.diag(Ktr) == 1.0)
+
+
+SCANS = {
+    # name: (m, d, gamma, budget, N_train, N_test)
+    "headline_m165_d1": (165, 1, 0.1, 1e-24, 6400, 0),
+    "config2_m50_d2": (50, 2, 0.1, 1e-24, 800, 200),
+    "config3_m100_d4": (100, 4, 0.1, 1e-16, 1600, 400),
+    "config5_m100_d5": (100, 5, 0.1, 1e-16, 64, 0),
+    "config5_m100_d6": (100, 6, 0.1, 1e-16, 64, 0),
+    "config5_m100_d7": (100, 7, 0.1, 1e-16, 64, 0),
+    "config5_m100_d8": (100, 8, 0.1, 1e-16, 64, 0),
+}
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", list(SCANS))
+def test_every_state_matches_oracle_bond_dims(name):
+    import paper_2411_09336_b200 as P
+
+    m, d, gamma, budget, n, mt = SCANS[name]
+    cfg = P.FeatureMapConfig(m, 2, d, gamma)
+    X = np.random.default_rng(0).uniform(0.0, 2.0, (n, m))
+    Xt = np.random.default_rng(1).uniform(0.0, 2.0, (mt, m))
+    rows = np.vstack([X, Xt]) if mt else X
+    rng = np.random.default_rng(2024)
+    sample = np.sort(rng.choice(n, min(n, 24), replace=False))
+    t0 = time.time()
+    ref_chi, ref_disc, ref_sites = oracle_states(rows, m, 2, d, gamma, budget, keep=sample)
+    t_oracle = time.time() - t0
+
+    t0 = time.time()
+    tr = P.simulate_dataset(X, cfg, budget=budget)
+    chi = tr.bond_dims()
+    disc = tr.discard.cpu().numpy()
+    if mt:
+        te = P.simulate_dataset(Xt, cfg, budget=budget)
+        chi = np.vstack([chi, te.bond_dims()])
+        disc = np.concatenate([disc, te.discard.cpu().numpy()])
+    K = P.compute_gram(tr, tr, "train").entries
+    t_gpu = time.time() - t0
+
+    flips = [int(i) for i in np.nonzero(np.any(chi != ref_chi, axis=1))[0]]
+    Ko = O.gram([ref_sites[i] for i in sample], [ref_sites[i] for i in sample], "train")
+    k_err = float(np.abs(K[np.ix_(sample, sample)] - Ko).max())
+    rec = {
+        "config": name, "m": m, "d": d, "gamma": gamma, "budget": budget, "states": int(rows.shape[0]),
+        "bond_dim_flips": len(flips), "flipped_rows": flips[:32],
+        "max_chi": int(chi.max()), "chi_capacity": int(tr.chi_cap),
+        "max_abs_discard_diff": float(np.abs(disc - ref_disc).max()),
+        "sampled_states": int(len(sample)), "max_abs_K_err_sampled_pairs": k_err,
+        "oracle_seconds": t_oracle, "oracle_processes": host_cores(), "gpu_seconds": t_gpu,
+    }
+    out = ROOT / "gpurun_out"
+    out.mkdir(exist_ok=True)
+    (out / f"scale_parity_{name}.json").write_text(json.dumps(rec, indent=1))
+    print(json.dumps(rec))
+    assert not flips, f"{len(flips)} of {rows.shape[0]} states differ in bond dims: {flips[:8]}"
+    assert k_err < _tol(budget)
+    assert np.array_equal(K, K.T) and np.all(np.diag(K) == 1.0)
