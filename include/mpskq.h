@@ -156,13 +156,17 @@ int mpskq_simulate(int m, int chi_cap, const int32_t* ops_dev, int64_t n_ops, in
  * coefficients sit in coef_dev).  phase_cycles_dev (nullable, n_states x 3
  * int64) receives the device clock cycles each state spent in
  * {canonicalize, one_qubit, two_qubit} ops (MpsState.timings keys,
- * mps.py:137, :159, :204).                                                */
+ * mps.py:137, :159, :204).  nominal_flops_dev (nullable, n_states doubles)
+ * receives the nominal flop count of the replayed ops (the
+ * simulation roofline numerator): per two-qubit gate theta 8*2chl*chm*2chr +
+ * gate 128*chl*chr + thin SVD 8*(4MN^2 + 8N^3) of the 2chl x 2chr theta;
+ * per QR move 16*M*N^2 + the R push 8*k*N*cols.                           */
 int mpskq_run_program(int m, int chi_cap, const int32_t* ops_dev, int64_t n_ops, int64_t n_gates,
                       const double* coef_dev, int64_t n_params, int64_t n_states, double budget,
                       int chi_max, const int64_t* site_off_dev, int64_t state_stride,
                       int from_input, double* sites_dev, int32_t* chi_dev, double* discard_dev,
                       int32_t* peak_chi_dev, int32_t* status_dev, int64_t* entry_log_dev,
-                      int64_t* phase_cycles_dev, void* stream);
+                      int64_t* phase_cycles_dev, double* nominal_flops_dev, void* stream);
 
 /* Move n states between chi-capacity layouts (mpskq_batch_layout): state i
  * of src (bond dims chi_dev row i) becomes row dst_rows_dev[i] of dst

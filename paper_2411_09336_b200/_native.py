@@ -65,7 +65,7 @@ _SIGNATURES = {
     "mpskq_run_program": (
         C.c_int,
         [C.c_int, C.c_int, _vp, C.c_int64, C.c_int64, _vp, C.c_int64, C.c_int64, C.c_double,
-         C.c_int, _vp, C.c_int64, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+         C.c_int, _vp, C.c_int64, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     ),
     "mpskq_relayout": (
         C.c_int,

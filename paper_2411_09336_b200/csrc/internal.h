@@ -52,6 +52,7 @@ struct SimArgs {
   void* scratch;  // set by the launcher (rotation logs of capacities > 32)
   int from_input = 0;                // continue the states already in sites/chi/discard/peak
   long long* phase_cycles = nullptr;  // n_states x {canonicalize, one_qubit, two_qubit}
+  double* nominal_flops = nullptr;    // n_states: nominal flop count of the replayed ops
 };
 int launch_simulate(const SimArgs& a, void* stream);
 
@@ -94,6 +95,7 @@ struct OverlapArgs {
   // row_ids_out[k].  Train rows hold only the entries the rank computed
   // (ordered i < j); mpskq_assemble_rows mirrors the rest on the gatherer.
   // ket_pos_out (nullable): ordered position of every ket (train mirror).
+  bool owned = false;
   double* rows_out = nullptr;
   int32_t* row_ids_out = nullptr;
   int32_t* ket_pos_out = nullptr;

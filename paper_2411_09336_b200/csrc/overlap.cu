@@ -699,7 +699,7 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
     return s_;
   }
   invert_perm_kernel<<<blocks_for(a.n_kets), threads, 0, st>>>(kperm, a.n_kets, static_cast<int32_t*>(kinv));
-  if (a.world > 1) cudaMemsetAsync(ordered, 0, elem * (size_t)a.n_bras * a.n_kets, st);
+  if (a.world > 1 && !a.owned) cudaMemsetAsync(ordered, 0, elem * (size_t)a.n_bras * a.n_kets, st);
   block_narrow_kernel<<<blocks_for(nbk * (m + 1)), threads, 0, st>>>(a.ket_chi, kperm, m, a.n_kets, nbk,
                                                                     static_cast<uint8_t*>(narrow));
   void *bra = nullptr, *ket = nullptr;
@@ -726,7 +726,7 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
       band_tiles.push_back((int64_t)tiles.size());
     }
   } else {
-    tiles = make_tiles(train, a.n_bras, a.n_kets, kWarpsO1, kLanes, a.rank, a.world, 0, -1, a.rows_out != nullptr);
+    tiles = make_tiles(train, a.n_bras, a.n_kets, kWarpsO1, kLanes, a.rank, a.world, 0, -1, a.owned);
     band_rows.push_back(a.n_bras);
     band_tiles.push_back((int64_t)tiles.size());
   }
@@ -835,7 +835,7 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
     overlap_o1_kernel<<<grid, kWarpsO1 * 32, smem, st>>>(o);
     const int32_t* bpos = train ? static_cast<const int32_t*>(kinv) : nullptr;
     const int rows = (int)std::min<int64_t>(a.n_bras, 148 * 32);
-    if (a.rows_out) {
+    if (a.owned) {
       const int64_t n_owned = owned_row_count(4, a.n_bras, a.rank, a.world);
       if (n_owned > 0)
         owned_rows_kernel<<<(int)std::min<int64_t>(n_owned, 148 * 32), 256, 0, st>>>(
@@ -867,11 +867,11 @@ int launch_mma(const OverlapArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(mma)");
   }
   const bool train = a.kind == MPSKQ_KIND_TRAIN;
-  auto tiles = make_tiles(train, a.n_bras, a.n_kets, 1, C::pairs, a.rank, a.world, 0, -1, a.rows_out != nullptr);
+  auto tiles = make_tiles(train, a.n_bras, a.n_kets, 1, C::pairs, a.rank, a.world, 0, -1, a.owned);
   int2* dtiles = nullptr;
   if (int s = upload_tiles(tiles, &dtiles, st)) return s;
   double* full = nullptr;  // row ownership: the rank's rows in a full-size buffer, then compacted
-  if (a.rows_out) {
+  if (a.owned && !tiles.empty()) {
     e = cudaMallocAsync(reinterpret_cast<void**>(&full), sizeof(double) * std::max<int64_t>(1, a.n_bras * a.n_kets), st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(owned rows)");
   }
@@ -938,7 +938,7 @@ int launch_overlap(const OverlapArgs& a, void* stream) {
     default: return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", a.chi_cap);
   }
   if (s != MPSKQ_OK) return s;
-  if (a.kind == MPSKQ_KIND_TRAIN && a.out_mode == MPSKQ_OUT_KERNEL && a.rank == 0 && !a.rows_out &&
+  if (a.kind == MPSKQ_KIND_TRAIN && a.out_mode == MPSKQ_OUT_KERNEL && a.rank == 0 && !a.owned &&
       !(a.host_out && a.chi_cap == 4 && a.world == 1)) {
     fill_diag_kernel<<<(int)std::min<int64_t>((a.n_bras + 255) / 256, 1024), 256, 0, st>>>(
         a.out, a.ld, a.n_bras);
@@ -1087,9 +1087,10 @@ extern "C" int mpskq_overlap_owned_rows(int kind, int m, int chi_cap, const int6
     return fail(MPSKQ_ERR_INVALID, "train kind requires bras and kets to be the same states");
   if (world < 1 || rank < 0 || rank >= world)
     return fail(MPSKQ_ERR_INVALID, "bad rank %d of world %d", rank, world);
-  if (!rows_out_dev || !row_ids_dev) return fail(MPSKQ_ERR_INVALID, "owned-row outputs are required");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t n_owned = owned_row_count(chi_cap, n_bras, rank, world);
+  if (n_owned > 0 && (!rows_out_dev || !row_ids_dev))
+    return fail(MPSKQ_ERR_INVALID, "owned-row outputs are required");
   if (n_owned > 0) {
     // padding rows of a short last band keep id -1 (skipped by the scatter)
     cudaError_t e = cudaMemsetAsync(row_ids_dev, 0xff, sizeof(int32_t) * n_owned, st);
@@ -1103,8 +1104,10 @@ extern "C" int mpskq_overlap_owned_rows(int kind, int m, int chi_cap, const int6
     if (e != cudaSuccess) return cuda_fail(e, "ket positions");
   }
   if (n_bras == 0 || n_kets == 0) return MPSKQ_OK;
+  if (n_owned == 0 && !ket_pos_dev) return MPSKQ_OK;  // nothing to compute on this rank
   OverlapArgs a{kind, MPSKQ_OUT_KERNEL, m, chi_cap, site_off_dev, state_stride, bra_sites_dev, bra_chi_dev,
                 n_bras, ket_sites_dev, ket_chi_dev, n_kets, rank, world, nullptr, n_kets};
+  a.owned = true;
   a.rows_out = rows_out_dev;
   a.row_ids_out = row_ids_dev;
   a.ket_pos_out = ket_pos_dev;

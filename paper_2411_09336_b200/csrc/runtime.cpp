@@ -355,7 +355,7 @@ int mpskq_run_program(int m, int chi_cap, const int32_t* ops_dev, int64_t n_ops,
                       int chi_max, const int64_t* site_off_dev, int64_t state_stride,
                       int from_input, double* sites_dev, int32_t* chi_dev, double* discard_dev,
                       int32_t* peak_chi_dev, int32_t* status_dev, int64_t* entry_log_dev,
-                      int64_t* phase_cycles_dev, void* stream) {
+                      int64_t* phase_cycles_dev, double* nominal_flops_dev, void* stream) {
   if (m < 1) return fail(MPSKQ_ERR_INVALID, "qubit count must be at least 1");
   if (!chi_cap_supported(chi_cap))
     return fail(MPSKQ_ERR_INVALID, "chi capacity %d is not compiled in", chi_cap);
@@ -367,6 +367,7 @@ int mpskq_run_program(int m, int chi_cap, const int32_t* ops_dev, int64_t n_ops,
             sites_dev, chi_dev, discard_dev,  peak_chi_dev, status_dev, entry_log_dev, nullptr};
   a.from_input = from_input != 0;
   a.phase_cycles = reinterpret_cast<long long*>(phase_cycles_dev);
+  a.nominal_flops = nominal_flops_dev;
   return launch_simulate(a, stream);
 }
 

@@ -31,6 +31,9 @@ namespace mpskq {
 __device__ constexpr double kNoiseFloor = 10.0 * DBL_EPSILON;
 // 1/sqrt(2) exactly as the reference rounds it: _H_MATRIX = [[1,1],[1,-1]]/sqrt(2)
 __device__ constexpr double kInvSqrt2 = 0.7071067811865475;
+#ifndef MPSKQ_NOISE_SCALE_N
+#define MPSKQ_NOISE_SCALE_N 1  // 0: round-1 threshold (A/B only)
+#endif
 constexpr int kMaxSweeps = 40;
 constexpr int kNoConvergence = 1 << 30;  // flag bit in jacobi()'s round count
 // Lanes (threads) per state by capacity.  Same-box A/B of the simulator
@@ -579,8 +582,8 @@ __device__ __noinline__ int jacobi_sweeps(Smem<CAP, NT>& sm, int Rr, int n) {
     const int c = idx / Rr, r = idx - c * Rr;
     fro += cnorm2(A[c * LD + r]);
   }
-  const double noise2 =
-      0.25 * DBL_EPSILON * DBL_EPSILON * block_sum<NT>(fro, sm.red) * (n > 100 ? 100.0 / n : 1.0);
+  const double noise2 = 0.25 * DBL_EPSILON * DBL_EPSILON * block_sum<NT>(fro, sm.red) *
+                        (MPSKQ_NOISE_SCALE_N && n > 100 ? 100.0 / n : 1.0);
   int round = 0, quiet = 0;
   for (; round < max_rounds;) {
     const int t = round % span;
@@ -810,7 +813,21 @@ struct StateCtx {
   int status;
   int peak;
   double discard;
+  double flops = 0.0;  // nominal LAPACK-style flop count, thread 0
 };
+
+// Nominal flops of one apply_two_qubit (fixed here once): theta
+// = site_q . site_{q+1} (8 * 2chl * chm * 2chr), the 4x4 gate (128 chl chr),
+// thin SVD of the (2chl x 2chr) theta, 8 (4 M N^2 + 8 N^3) with M >= N.
+__device__ __forceinline__ double nominal_two_qubit(int chl, int chm, int chr) {
+  const double a = 2.0 * chl, b = 2.0 * chr, M = fmax(a, b), N = fmin(a, b);
+  return 8.0 * a * chm * b + 128.0 * chl * chr + 8.0 * (4.0 * M * N * N + 8.0 * N * N * N);
+}
+// one QR move: Householder QR of an (M x N) matrix 8 * 2 M N^2 plus the R push
+// into the neighbour (8 * k * N * cols)
+__device__ __forceinline__ double nominal_qr(int M, int N, int k, int cols) {
+  return 16.0 * M * (double)N * N + 8.0 * k * (double)N * cols;
+}
 
 template <int CAP, int NT>
 __device__ void op_one_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, double2 cs,
@@ -882,7 +899,10 @@ __device__ void op_qr_left(Smem<CAP, NT>& sm, StateCtx& st, int i) {
     N[idx] = acc;
   }
   bsync<NT>();
-  if (tid == 0) sm.chi[i + 1] = k;
+  if (tid == 0) {
+    sm.chi[i + 1] = k;
+    st.flops += nominal_qr(Rr, chr, k, cols);
+  }
   bsync<NT>();
 }
 
@@ -921,7 +941,10 @@ __device__ void op_qr_right(Smem<CAP, NT>& sm, StateCtx& st, int i) {
     P[idx] = acc;
   }
   bsync<NT>();
-  if (tid == 0) sm.chi[i] = k;
+  if (tid == 0) {
+    sm.chi[i] = k;
+    st.flops += nominal_qr(Rr, chl, k, rows);
+  }
   bsync<NT>();
 }
 
@@ -1117,6 +1140,7 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
     sm.chi[q + 1] = keep;
     st.discard += sm.scal[1];  // accumulated_discard (mps.py:201)
     st.peak = max(st.peak, keep);
+    st.flops += nominal_two_qubit(chl, chm, chr);
   }
   bsync<NT>();
   MPSKQ_DBG_ADD(6, t_wside);
@@ -1235,6 +1259,7 @@ __global__ void __launch_bounds__(NT * SpcFor<NT>::value) sim_kernel(SimArgs a) 
         a.discard[n] = st.discard;
         a.peak[n] = st.peak;
         a.status[n] = st.status;
+        if (a.nominal_flops) a.nominal_flops[n] = st.flops;
         if (a.phase_cycles) {
           a.phase_cycles[3 * n] = ph_canon;
           a.phase_cycles[3 * n + 1] = ph_one;

@@ -230,6 +230,7 @@ class MpsBatch(Sequence):
         self.entry_log = entry_log
         self.seconds = seconds
         self.phase_cycles = None  # int64 (n, 3) device clocks per phase (simulate_program)
+        self.nominal_flops = None  # float64 (n,) nominal simulation flops
         self._phase_host = None
         self._host = None
 
@@ -395,6 +396,7 @@ def simulate_program(prog: Program, coef, budget: float, chi_max: int = 0,
             status=torch.zeros(nl, dtype=torch.int32, device=dev),
             elog=torch.zeros((nl, prog.n_gates), dtype=torch.int64, device=dev) if memory_log else None,
             phase=torch.zeros((nl, 3), dtype=torch.int64, device=dev),
+            flops=torch.zeros(nl, dtype=torch.float64, device=dev),
         )
         with Timer() as tm:
             N.check(
@@ -402,7 +404,7 @@ def simulate_program(prog: Program, coef, budget: float, chi_max: int = 0,
                     m, cap, dptr(ops_d), prog.ops.shape[0], prog.n_gates, dptr(coef_l), prog.n_params, nl,
                     float(budget), int(chi_max), dptr(off_d), stride, 0, dptr(lv["sites"]), dptr(lv["chi"]),
                     dptr(lv["disc"]), dptr(lv["peak"]), dptr(lv["status"]), dptr(lv["elog"]),
-                    dptr(lv["phase"]), stream_ptr(),
+                    dptr(lv["phase"]), dptr(lv["flops"]), stream_ptr(),
                 )
             )
         seconds += tm.seconds()
@@ -425,12 +427,14 @@ def simulate_program(prog: Program, coef, budget: float, chi_max: int = 0,
     fin = levels[-1]
     if len(levels) == 1:
         sites, chi, disc, peak, elog, phase = (fin[k] for k in ("sites", "chi", "disc", "peak", "elog", "phase"))
+        flops = fin["flops"]
     else:
         sites = torch.empty((n, 2 * fin["stride"]), dtype=torch.float64, device=dev)
         chi = torch.empty((n, m + 1), dtype=torch.int32, device=dev)
         disc = torch.empty(n, dtype=torch.float64, device=dev)
         peak = torch.empty(n, dtype=torch.int32, device=dev)
         phase = torch.empty((n, 3), dtype=torch.int64, device=dev)
+        flops = torch.zeros(n, dtype=torch.float64, device=dev)
         elog = torch.empty((n, prog.n_gates), dtype=torch.int64, device=dev) if memory_log else None
         for lv in levels:  # later levels overwrite the rows that overflowed earlier ones
             r32 = None if lv["rows"] is None else lv["rows"].to(torch.int32)
@@ -442,11 +446,13 @@ def simulate_program(prog: Program, coef, budget: float, chi_max: int = 0,
             disc.index_copy_(0, idx, lv["disc"])
             peak.index_copy_(0, idx, lv["peak"])
             phase.index_copy_(0, idx, lv["phase"])
+            flops.index_add_(0, idx, lv["flops"])  # nominal work of every level a state ran at
             if elog is not None:
                 elog.index_copy_(0, idx, lv["elog"])
     batch = MpsBatch(m, fin["cap"], fin["off"], fin["stride"], sites, chi, disc, peak, budget, prog.gate_count_1q,
                      prog.gate_count_2q, prog.final_center, elog, seconds)
     batch.phase_cycles = phase
+    batch.nominal_flops = flops
     return batch
 
 
@@ -514,7 +520,7 @@ def _evolve(state: MpsState, ops: list, coef: np.ndarray, n_gates: int = 0, memo
         N.check(N.lib().mpskq_run_program(
             state.m, cap, dptr(ops_d), len(ops), max(n_gates, 1), dptr(coef_d), n_params, 1,
             float(state.trunc_budget_per_gate), 0, dptr(b.site_off_dev), b.stride, 1, dptr(b.sites), dptr(b.chi),
-            dptr(b.discard), dptr(b.peak), dptr(status), dptr(elog), dptr(phase), stream_ptr()))
+            dptr(b.discard), dptr(b.peak), dptr(status), dptr(elog), dptr(phase), None, stream_ptr()))
         if _check_states(status.cpu().numpy()).size:
             continue
         b.phase_cycles = phase

@@ -1,6 +1,7 @@
 """Secondary measurements for the non-headline BASELINE configs (parity cases,
 not bench lines): per config, device time of simulate + train kernel with
-CUDA events, algorithmic overlap flops and the FP64 fraction."""
+CUDA events, algorithmic overlap flops, nominal simulation flops, and the
+fractions of the measured FP64 peak (mpskq_fp64_probe, as in bench.py)."""
 import json
 import sys
 from pathlib import Path
@@ -46,7 +47,11 @@ def timed(fn, reps=2):
 
 
 def main(names):
-    res = {}
+    from bench import fp64_peak_tflops
+    from paper_2411_09336_b200 import _native as N
+
+    peak = fp64_peak_tflops(N.lib(), torch)
+    res = {"fp64_peak_tflops_measured": peak}
     for name in names:
         m, d, gamma, budget, n = CONFIGS[name]
         cfg = P.FeatureMapConfig(m, 2, d, gamma)
@@ -60,10 +65,18 @@ def main(names):
         K, ov_ms = timed(lambda: overlap_matrix(batch, batch, "train"), reps=2)
         chi = batch.bond_dims()
         fl = train_flops(chi)
+        # nominal simulation flops (theta + gate + LAPACK-nominal
+        # thin SVD + QR moves, counted by the simulator per state) over the
+        # measured simulation time; escalated states count every level they ran
+        sim_fl = float(batch.nominal_flops.sum().item())
         ent = n * (n - 1) / 2
         r = {"N": n, "chi_cap": batch.chi_cap, "chi_max": int(chi.max()), "peak_max": int(batch.peak.max()),
-             "sim_ms": sim_ms, "mps_states_per_s": n / (sim_ms / 1e3), "overlap_ms": ov_ms,
+             "sim_ms": sim_ms, "mps_states_per_s": n / (sim_ms / 1e3),
+             "sim_nominal_flops": sim_fl, "sim_tflops_nominal": sim_fl / (sim_ms / 1e3) / 1e12,
+             "overlap_ms": ov_ms,
              "entries_per_s": ent / (ov_ms / 1e3), "overlap_tflops_alg": fl / (ov_ms / 1e3) / 1e12}
+        r["overlap_frac_of_fp64_peak"] = r["overlap_tflops_alg"] / peak
+        r["sim_frac_of_fp64_peak"] = r["sim_tflops_nominal"] / peak
         res[name] = r
         print(name, json.dumps(r), flush=True)
     return res

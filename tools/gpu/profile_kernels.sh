@@ -1,0 +1,22 @@
+# ncu captures of the secondary-config kernels (one launch each):
+# overlap_mma_kernel at capacities 8 / 12 / 24 / 96 (--set full) and
+# sim_kernel at 24 / 48 (--set full) and 96 / 128 (a reduced section set:
+# one launch runs for seconds, and --set full replays it ~40 times).
+mkdir -p gpurun_out/ncu
+run() {  # name config n kernel-regex extra-ncu-args...
+  local name=$1 cfg=$2 n=$3 k=$4; shift 4
+  timeout 900 ncu --clock-control none --import-source on --kernel-name-base demangled -k "regex:$k" -c 1 "$@" \
+      -o gpurun_out/ncu/$name --force-overwrite python tools/prof_configs.py $cfg --n $n \
+      > gpurun_out/ncu/$name.log 2>&1
+  echo "$name rc=$?"
+}
+for c in "mma8 c5_d2_cap8 512 overlap_mma_kernel<8>" "mma12 c2_cap12 512 overlap_mma_kernel<12>" \
+         "mma24 c3_cap24 256 overlap_mma_kernel<24>" "mma96 c5_d8_cap96 64 overlap_mma_kernel<96>"; do
+  set -- $c
+  run $1 $2 $3 "$4" --set full
+done
+run sim24 c3_cap24 148 "sim_kernel<24" --set full
+run sim48 c5_d6_cap48 148 "sim_kernel<48" --set full
+run sim96 c5_d8_cap96 64 "sim_kernel<96" --section SpeedOfLight --section WarpStateStats --section Occupancy --section LaunchStats
+run sim128 s6_b24_cap128 16 "sim_kernel<128" --section SpeedOfLight --section WarpStateStats --section Occupancy --section LaunchStats
+ls -la gpurun_out/ncu

@@ -1,6 +1,10 @@
-set -x
+# GPU test suite (fast part, verbose), then the default bench line.
+mkdir -p gpurun_out
 nproc
-python -m pytest tests -m gpu -q -p no:cacheprovider -rf --durations=25 > gpurun_out/r2_gpu_tests_1.log 2>&1
-tail -5 gpurun_out/r2_gpu_tests_1.log
-python bench.py --steps 5 --warmup 3 --cpu-seconds 5 > gpurun_out/r2_bench_1.json 2> gpurun_out/r2_bench_1.err
-tail -c 3000 gpurun_out/r2_bench_1.json
+timeout 1500 python -m pytest tests -m "gpu and not slow" -v -p no:cacheprovider -rf --durations=20 \
+  > gpurun_out/r2_gpu_tests_fast.log 2>&1
+echo "fast tests rc=$?"
+grep -E "FAILED|ERROR|passed|failed" gpurun_out/r2_gpu_tests_fast.log | tail -15
+timeout 900 python bench.py --steps 5 --warmup 3 --cpu-seconds 5 > gpurun_out/r2_bench_1.json 2> gpurun_out/r2_bench_1.err
+echo "bench rc=$?"
+tail -c 1500 gpurun_out/r2_bench_1.err
