@@ -555,6 +555,32 @@ def gpu_main(args) -> None:
 
 
 # ------------------------------------------------------------------ reference arm
+def as_shipped_sample(rows: int) -> dict | None:
+    """The unmodified reference as shipped (BASELINE.md section 2 mode 1):
+    kernel.run_distributed(k=1) from baseline/_ref on `rows` headline rows
+    (its worker threads are GIL-bound, k > 1 is slower), entries/s."""
+    ref = ROOT / "baseline" / "_ref"
+    if rows <= 1 or not (ref / "mpskernel").exists():
+        return None
+    import importlib
+
+    sys.path.insert(0, str(ref))
+    try:
+        K = importlib.import_module("mpskernel.kernel")
+        A = importlib.import_module("mpskernel.ansatz")
+        X = feature_rows(rows)
+        cfg = A.FeatureMapConfig(M, R, D, GAMMA)
+        t0 = time.perf_counter()
+        K.run_distributed(X, X, cfg, K.make_schedule(rows, rows, 1, "round_robin", "train"), budget=BUDGET)
+        dt = time.perf_counter() - t0
+    finally:
+        sys.path.remove(str(ref))
+    entries = rows * (rows - 1) / 2
+    return {"value": entries / dt, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"mpskernel.kernel.run_distributed(k=1), unmodified, on {rows} headline rows "
+                      f"({rows} simulations + {int(entries)} overlaps in {dt:.1f} s)"}
+
+
 def reference_main(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -572,6 +598,7 @@ def reference_main(args) -> None:
         walls.append(s["projected_train_wall_s"])
     elapsed = (time.perf_counter() - t0) / args.steps
     v = float(np.median(vals))
+    shipped = as_shipped_sample(args.shipped_rows)
     line = {
         "metric": METRIC,
         "impl": "reference",
@@ -590,8 +617,10 @@ def reference_main(args) -> None:
         "train_wall_s": float(np.median(walls)),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": s["cores"], "kind": "port", "sample": s["sample"]},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "as_shipped": shipped,
         "note": "reference is pure Python/numpy (nothing to compile); timed through oracle/mps_oracle.py, "
-                "which is bitwise identical to it (tests/test_oracle.py)",
+                "which is bitwise identical to it (tests/test_oracle.py), in a process pool over every host "
+                "core; `as_shipped` times the unmodified reference's own run_distributed(k=1) from baseline/_ref",
     }
     print(json.dumps(line), flush=True)
 
@@ -607,6 +636,7 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=8.0)
+    ap.add_argument("--shipped-rows", type=int, default=48, help="rows of the as-shipped reference sample (0: skip)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -314,8 +314,9 @@ def compute_gram(bras, kets, kind: str, report: RunReport | None = None) -> Gram
     if kind not in KINDS:
         raise ValueError(f"kind must be one of {KINDS}")
     if kind == "train":
-        same = bras is kets or (
-            not isinstance(bras, MpsBatch) and len(bras) == len(kets) and all(a is b for a, b in zip(bras, kets))
+        same = bras is kets or (isinstance(bras, MpsBatch) and bras.same_states(kets)) or (
+            not isinstance(bras, MpsBatch) and not isinstance(kets, MpsBatch) and len(bras) == len(kets)
+            and all(a is b for a, b in zip(bras, kets))
         )
         if not same:
             raise ValueError("train kind requires bras and kets to be the same states")

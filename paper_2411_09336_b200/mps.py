@@ -229,6 +229,7 @@ class MpsBatch(Sequence):
         self.ortho_center = ortho_center
         self.entry_log = entry_log
         self.seconds = seconds
+        self._root, self._base, self._items = self, 0, {}  # row views share the root's item cache
         self.phase_cycles = None  # int64 (n, 3) device clocks per phase (simulate_program)
         self.nominal_flops = None  # float64 (n,) nominal simulation flops
         self._phase_host = None
@@ -252,20 +253,38 @@ class MpsBatch(Sequence):
 
     def __getitem__(self, i):
         if isinstance(i, slice):
-            return [self[k] for k in range(*i.indices(len(self)))]
+            a, b, step = i.indices(len(self))
+            if step == 1:  # a device view, like slicing the reference's list of states
+                return self.rows(a, max(a, b))
+            return [self[k] for k in range(a, b, step)]
         n = len(self)
         if i < 0:
             i += n
         if not 0 <= i < n:
             raise IndexError(i)
+        # one host MpsState object per state (list semantics: batch[i] is batch[i],
+        # which compute_gram's train check relies on, kernel.py:161-164).  The
+        # object is a host copy: mutating it does not change the device batch.
+        key = self._base + i
+        hit = self._root._items.get(key)
+        if hit is not None:
+            return hit
         sites, chi, disc, peak = self._host_arrays()
         row, c = sites[i], chi[i]
         ts = [
             row[self.site_off[s] : self.site_off[s] + c[s] * 2 * c[s + 1]].reshape(c[s], 2, c[s + 1]).copy()
             for s in range(self.m)
         ]
-        return MpsState(ts, self.budget, float(disc[i]), self.ortho_center, int(peak[i]), self.gate_count_1q,
-                        self.gate_count_2q, self.timings(i))
+        st = MpsState(ts, self.budget, float(disc[i]), self.ortho_center, int(peak[i]), self.gate_count_1q,
+                      self.gate_count_2q, self.timings(i))
+        self._root._items[key] = st
+        return st
+
+    def same_states(self, other) -> bool:
+        """True when `other` views exactly the same states (the batch analogue
+        of the reference's element-wise `is` check)."""
+        return (isinstance(other, MpsBatch) and other._root is self._root and other._base == self._base
+                and len(other) == len(self))
 
     def timings(self, i: int) -> dict:
         """Per-phase device seconds of state i (MpsState.timings keys,
@@ -284,6 +303,8 @@ class MpsBatch(Sequence):
                        self.discard[a:b], self.peak[a:b], self.budget, self.gate_count_1q,
                        self.gate_count_2q, self.ortho_center, log, self.seconds * (b - a) / max(len(self), 1))
         out.phase_cycles = None if self.phase_cycles is None else self.phase_cycles[a:b]
+        out.nominal_flops = None if self.nominal_flops is None else self.nominal_flops[a:b]
+        out._root, out._base = self._root, self._base + a
         return out
 
     def to_states(self) -> list:

@@ -10,13 +10,13 @@ run() {  # name config n kernel-regex extra-ncu-args...
       > gpurun_out/ncu/$name.log 2>&1
   echo "$name rc=$?"
 }
-for c in "mma8 c5_d2_cap8 512 overlap_mma_kernel<8>" "mma12 c2_cap12 512 overlap_mma_kernel<12>" \
-         "mma24 c3_cap24 256 overlap_mma_kernel<24>" "mma96 c5_d8_cap96 64 overlap_mma_kernel<96>"; do
+for c in "mma8 c5_d2_cap8 512 overlap_mma_kernel<.int.8>" "mma12 c2_cap12 512 overlap_mma_kernel<.int.12>" \
+         "mma24 c3_cap24 256 overlap_mma_kernel<.int.24>" "mma96 c5_d8_cap96 64 overlap_mma_kernel<.int.96>"; do
   set -- $c
   run $1 $2 $3 "$4" --set full
 done
-run sim24 c3_cap24 148 "sim_kernel<24" --set full
-run sim48 c5_d6_cap48 148 "sim_kernel<48" --set full
-run sim96 c5_d8_cap96 64 "sim_kernel<96" --section SpeedOfLight --section WarpStateStats --section Occupancy --section LaunchStats
-run sim128 s6_b24_cap128 16 "sim_kernel<128" --section SpeedOfLight --section WarpStateStats --section Occupancy --section LaunchStats
+run sim24 c3_cap24 148 "sim_kernel<.int.24," --set full
+run sim48 c5_d6_cap48 148 "sim_kernel<.int.48," --set full
+run sim96 c5_d8_cap96 64 "sim_kernel<.int.96," --section SpeedOfLight --section WarpStateStats --section Occupancy --section LaunchStats
+run sim128 s6_b24_cap128 16 "sim_kernel<.int.128," --section SpeedOfLight --section WarpStateStats --section Occupancy --section LaunchStats
 ls -la gpurun_out/ncu
