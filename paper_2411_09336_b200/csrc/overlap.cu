@@ -262,10 +262,6 @@ inline size_t o1_smem_bytes(int m) {
          sizeof(int32_t) * kWarpsO1 * (size_t)(m + 1);
 }
 
-// ceil(2^32 / m): exact q / m via __umulhi for q < 2^32 / m (the per-CTA
-// site counter stays below 2^24 for any launch this library makes)
-inline uint32_t o1_magic(int m) { return (uint32_t)((((uint64_t)1 << 32) + (uint64_t)m - 1) / (uint64_t)m); }
-
 struct O1Args {
   const double2* bra;  // [site][n_pad_bra][entry]
   const double2* ket;  // [site][nblk_ket][entry][lane]
@@ -279,7 +275,6 @@ struct O1Args {
   const int32_t* bperm;      // ordered position -> bra index (nullable)
   const int32_t* kperm;      // ordered position -> ket index
   const uint8_t* kb_narrow;  // [ket block][bond]: block max chi <= 3
-  uint32_t m_magic;          // ceil(2^32 / m): q / m = umulhi(q, m_magic) for q < 2^32 / m
 };
 
 // One CTA = 8 bras (warps) x 32 kets (lanes); one thread owns one pair's 4x4
@@ -301,9 +296,6 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
   int32_t* schi = reinterpret_cast<int32_t*>(ld_ctr + 4);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m = a.m;
-  // 32-bit shared addresses of the ring, computed once
-  const uint32_t sket_u = smem_u32(sket), sbra_u = smem_u32(sbra);
-  const uint32_t full_u = smem_u32(full), empty_u = smem_u32(empty);
   if (tid == 0) {
     for (int q = 0; q < kStages; ++q) {
       mbar_init(&full[q], 1);
@@ -320,15 +312,14 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
   const int64_t bstride = a.n_pad_bra * kEnt;
   uint32_t it = 0;  // sites this warp consumed (ring position + phase)
   auto issue = [&](uint32_t q) {
-    const uint32_t tk = __umulhi(q, a.m_magic);  // q / m without a division
-    const int site = (int)(q - tk * (uint32_t)m);
-    const int2 tl = a.tiles[blockIdx.x + (int64_t)tk * gridDim.x];
+    const int2 tl = a.tiles[blockIdx.x + (int64_t)(q / m) * gridDim.x];
+    const int site = (int)(q % m);
     const uint32_t buf = q & (kStages - 1);
-    const uint32_t fb = full_u + buf * (uint32_t)sizeof(uint64_t);
-    mbar_arrive_expect_tx_u32(fb, kKetBytes + kBraBytes);
-    bulk_g2s_u32(sket_u + buf * kKetBytes, a.ket + (int64_t)tl.y * kEnt * kLanes + site * kstride, kKetBytes, fb);
-    bulk_g2s_u32(sbra_u + buf * kBraBytes, a.bra + (int64_t)tl.x * kWarpsO1 * kEnt + site * bstride, kBraBytes,
-                 fb);
+    mbar_arrive_expect_tx(&full[buf], kKetBytes + kBraBytes);
+    bulk_g2s(sket + buf * kEnt * kLanes, a.ket + (int64_t)tl.y * kEnt * kLanes + site * kstride,
+             kKetBytes, &full[buf]);
+    bulk_g2s(sbra + buf * kWarpsO1 * kEnt, a.bra + (int64_t)tl.x * kWarpsO1 * kEnt + site * bstride,
+             kBraBytes, &full[buf]);
   };
   // Lane 0 of every warp produces: refill free slots opportunistically (the
   // fastest warp keeps the ring full) and block only for the slot this warp
@@ -344,11 +335,10 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
       if (q >= total || q >= it + kStages) break;
       if (q >= kStages) {
         const uint32_t par = ((q / kStages) - 1) & 1;
-        const uint32_t eb = empty_u + (q & (kStages - 1)) * (uint32_t)sizeof(uint64_t);
         if (q <= it) {
-          mbar_wait_u32(eb, par);
+          mbar_wait(&empty[q & (kStages - 1)], par);
         } else {
-          const int ok = __shfl_sync(kFull, (int)mbar_test_u32(eb, par), 0);
+          const int ok = __shfl_sync(kFull, (int)mbar_test(&empty[q & (kStages - 1)], par), 0);
           if (!ok) break;
         }
       }
@@ -356,9 +346,7 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
       __syncwarp();
     }
   };
-  // per warp: bond b of this warp's bra in the low byte, the ket block's
-  // "max chi <= 3" flag of bond b in bit 8 (one shared load per site)
-  int32_t* mycn = schi + warp * (m + 1);
+  int32_t* mychi = schi + warp * (m + 1);
   for (int64_t k = 0; k < my_tiles; ++k) {
     const int2 tile = a.tiles[blockIdx.x + k * gridDim.x];
     const int64_t i = (int64_t)tile.x * kWarpsO1 + warp;  // bra (warp-uniform)
@@ -366,27 +354,24 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
     const int64_t ic = i < a.n_bras ? i : a.n_bras - 1;
     const int64_t ib = a.bperm ? a.bperm[ic] : ic;  // bra index of this warp
     const uint8_t* narrow = a.kb_narrow + (int64_t)tile.y * (m + 1);
-    for (int b = lane; b <= m; b += kLanes)
-      mycn[b] = __ldg(a.bra_chi + ib * (m + 1) + b) | ((int32_t)__ldg(narrow + b) << 8);
+    for (int b = lane; b <= m; b += kLanes) mychi[b] = __ldg(a.bra_chi + ib * (m + 1) + b);
     __syncwarp();
     double2 env[kP][kP];
 #pragma unroll
     for (int x = 0; x < kP; ++x)
 #pragma unroll
       for (int y = 0; y < kP; ++y) env[x][y] = make_double2(x == 0 && y == 0 ? 1.0 : 0.0, 0.0);
-    int na = 1;                          // chi_s of the bra (warp-uniform)
-    bool nar_l = (mycn[0] >> 8) != 0;  // ket block narrow at bond s
+    int na = 1;  // chi_s of the bra (warp-uniform)
     for (int s = 0; s < m; ++s) {
       // the counter only grows: run the producer when this warp's view of the
       // ring is less than half full (or its next slot may not be issued yet)
       if (seen < it + kStages / 2 + 1 && seen < total) produce();
-      const int cn1 = mycn[s + 1];
-      const int na1 = cn1 & 0xff;
-      const bool nar_r = (cn1 >> 8) != 0;
+      const int na1 = mychi[s + 1];
       const uint32_t buf = it & (kStages - 1);
-      mbar_wait_u32(full_u + buf * (uint32_t)sizeof(uint64_t), (it / kStages) & 1);
+      mbar_wait(&full[buf], (it / kStages) & 1);
       const double2* B = sket + buf * kEnt * kLanes + lane;  // B[e] at B[e * 32]
       const double2* A = sbra + buf * kWarpsO1 * kEnt + warp * kEnt;
+      const bool nar_l = __ldg(narrow + s) != 0, nar_r = __ldg(narrow + s + 1) != 0;
       double2 T[kP][2][kP];
       using namespace o1;
       switch (na) {
@@ -397,10 +382,9 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
       }
       o1_phase2(A, T, na, na1, nar_r, env);
       __syncwarp();
-      if (lane == 0) mbar_arrive_u32(empty_u + buf * (uint32_t)sizeof(uint64_t));
+      if (lane == 0) mbar_arrive(&empty[buf]);
       ++it;
       na = na1;
-      nar_l = nar_r;
     }
     const bool train = a.kind == MPSKQ_KIND_TRAIN;
     // results go to the ordered index space (full-sector tile rows); a gather
@@ -793,7 +777,7 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
         O1Args o{static_cast<const double2*>(bra), static_cast<const double2*>(ket), a.bra_chi,
                  a.n_bras, a.n_kets, npb, nbk, m, a.kind,
                  a.out_mode, dtiles + band_tiles[b], nt, static_cast<double*>(ordered), a.n_kets,
-                 bperm, kperm, static_cast<const uint8_t*>(narrow), o1_magic(m)};
+                 bperm, kperm, static_cast<const uint8_t*>(narrow)};
         overlap_o1_kernel<<<(int)std::min<int64_t>(nt, sms), kWarpsO1 * 32, smem, sb>>>(o);
       }
       cudaEventRecord(evs[b], sb);
@@ -842,7 +826,7 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
     O1Args o{static_cast<const double2*>(bra), static_cast<const double2*>(ket), a.bra_chi,
              a.n_bras, a.n_kets, npb, nbk, m, a.kind,
              a.out_mode, dtiles, (int64_t)tiles.size(), static_cast<double*>(ordered), a.n_kets,
-             bperm, kperm, static_cast<const uint8_t*>(narrow), o1_magic(m)};
+             bperm, kperm, static_cast<const uint8_t*>(narrow)};
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
