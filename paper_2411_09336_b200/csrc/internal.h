@@ -100,6 +100,8 @@ struct OverlapArgs {
   int32_t* row_ids_out = nullptr;
   int32_t* ket_pos_out = nullptr;
 };
+// overlap tile shape (bra rows x ket columns) of a capacity
+void tile_shape(int chi_cap, int* rb, int* cb);
 // rows of n_bras owned by `rank` under row ownership for this capacity
 int64_t owned_row_count(int chi_cap, int64_t n_bras, int rank, int world);
 int launch_overlap(const OverlapArgs& a, void* stream);

@@ -355,9 +355,11 @@ def run_distributed(X_bras, X_kets, cfg: FeatureMapConfig, schedule: TileSchedul
     X_kets = _check_rows(X_kets, cfg.m)
     if (X_bras.shape[0], X_kets.shape[0]) != (schedule.n_bras, schedule.n_kets):
         raise ValueError("schedule was built for different state counts")
-    if schedule.kind == "train" and not np.array_equal(X_bras, X_kets):
+    same = X_bras is X_kets or (X_bras.shape == X_kets.shape and X_bras.ctypes.data == X_kets.ctypes.data
+                                and X_bras.strides == X_kets.strides)
+    if schedule.kind == "train" and not same and not np.array_equal(X_bras, X_kets):
         raise ValueError("train kind requires identical bra and ket rows")
-    for X in (X_bras, X_kets):
+    for X in ((X_bras,) if same else (X_bras, X_kets)):
         if not np.all(np.isfinite(X)):
             raise ValueError("features must be finite")
     from . import distributed

@@ -57,7 +57,7 @@ def main(names):
         cfg = P.FeatureMapConfig(m, 2, d, gamma)
         X = np.random.default_rng(0).uniform(0.0, 2.0, (n, m))
         try:
-            batch, sim_ms = timed(lambda: simulate_rows(X, cfg, budget), reps=1)
+            batch, sim_ms = timed(lambda: simulate_rows(X, cfg, budget), reps=2 if n * m < 1e6 else 1)
         except RuntimeError as exc:
             res[name] = {"error": str(exc)}
             print(name, "ERROR", exc, flush=True)
