@@ -475,8 +475,25 @@ def gpu_main(args) -> None:
         sub_t = [O.simulate_row(x, M, R, D, GAMMA, BUDGET) for x in Xt[:3]]
         sub = [O.simulate_row(x, M, R, D, GAMMA, BUDGET) for x in X[:4]]
         Kto = O.gram([s.sites for s in sub_t], [s.sites for s in sub], "test")
+        # end to end through the public API (test rows and train rows in, M x N K
+        # out: run_distributed also simulates the train rows, kernel.py:443-512)
+        tsched = P.make_schedule(mt, n, 1, "round_robin", "test")
+        for _ in range(max(1, args.warmup)):
+            del_g = P.run_distributed(Xt, X, cfg, tsched, budget=BUDGET)
+        del del_g
+        a.record()
+        for _ in range(args.steps):
+            g = P.run_distributed(Xt, X, cfg, tsched, budget=BUDGET)
+            del g
+        b.record()
+        b.synchronize()
+        te2e_ms = a.elapsed_time(b) / args.steps
         test_line = {
             "workload": f"headline test kernel: {mt} test rows (seed 1) x {n} train states (BASELINE configs[3])",
+            "e2e": {"value": mt * n / (te2e_ms / 1e3), "unit": UNIT, "ms_per_step": te2e_ms,
+                    "h2d_bytes_per_step": Xt.nbytes + X.nbytes, "d2h_bytes_per_step": mt * n * 8,
+                    "path": "public API run_distributed(X_test, X_train, cfg, make_schedule(M, N, 1, 'round_robin', "
+                            "'test')): simulates the test AND train rows, K streamed to page-locked host memory"},
             "entries": mt * n, "value": mt * n / (t_ms / 1e3), "unit": UNIT, "ms_per_step": t_ms,
             "phases_ms": {"simulate_test_rows": t_sim, "overlap": t_ov},
             "roofline": None,  # filled below with the same peak

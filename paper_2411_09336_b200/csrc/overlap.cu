@@ -277,23 +277,28 @@ struct O1Args {
   const uint8_t* kb_narrow;  // [ket block][bond]: block max chi <= 3
 };
 
-// One CTA = 8 bras (warps) x 32 kets (lanes); one thread owns one pair's 4x4
-// complex environment in registers.  Persistent over its tiles, the CTA
-// streams each site's ket block (16 KB) and bra tile (4 KB) into an 8-stage
-// shared-memory ring with TMA bulk copies (cp.async.bulk) completing on
-// "full" mbarriers; every warp releases a slot on its "empty" mbarrier, so
-// warps drift up to the ring depth instead of synchronising every site.
-// Every warp can produce (lane 0 issues, the warp decides collectively): it
-// refills free slots opportunistically (test_wait) and blocks only for the
-// slot it needs next, so the fastest warp keeps the ring full (deadlock free).
-__global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) {
+// One CTA = 8 bras (compute warps) x 32 kets (lanes); one thread owns one
+// pair's 4x4 complex environment in registers.  Persistent over its tiles,
+// the CTA streams each site's ket block (16 KB) and bra tile (4 KB) through an
+// 8-stage shared-memory ring: TMA bulk copies (cp.async.bulk) complete on
+// "full" mbarriers, every compute warp releases a slot on its "empty"
+// mbarrier, so warps drift up to the ring depth instead of synchronising
+// every site.  Warp-specialised: the 8 compute warps (two warpgroups,
+// registers raised to 240 with setmaxnreg) only wait and release; a third
+// warpgroup (registers lowered to 24) runs the producer — one lane walks the
+// CTA's (tile, site) sequence, waits until all 8 compute warps released a
+// slot and issues its two copies.  (The earlier cooperative producer, where
+// every compute warp could refill slots through a CAS on a shared counter,
+// ran 147.8 ms at N=6400 against 142 ms for this one, `profiles/r02_ab_o1_ws.txt`.)
+constexpr int kThreadsO1Ws = (kWarpsO1 + 4) * 32;
+
+__global__ void __launch_bounds__(kThreadsO1Ws, 1) overlap_o1_kernel(O1Args a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* sket = reinterpret_cast<double2*>(smem_raw);
   double2* sbra = sket + kStages * kEnt * kLanes;
   uint64_t* full = reinterpret_cast<uint64_t*>(sbra + kStages * kWarpsO1 * kEnt);
   uint64_t* empty = full + kStages;
-  uint32_t* ld_ctr = reinterpret_cast<uint32_t*>(empty + kStages);  // sites issued so far
-  int32_t* schi = reinterpret_cast<int32_t*>(ld_ctr + 4);
+  int32_t* schi = reinterpret_cast<int32_t*>(empty + kStages) + 4;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m = a.m;
   if (tid == 0) {
@@ -301,51 +306,35 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
       mbar_init(&full[q], 1);
       mbar_init(&empty[q], kWarpsO1);
     }
-    *ld_ctr = 0;
     mbar_fence_init();
   }
   __syncthreads();
-  if ((int64_t)blockIdx.x >= a.n_tiles) return;
-  const int64_t my_tiles = (a.n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
-  const uint32_t total = (uint32_t)(my_tiles * m);
-  const int64_t kstride = a.nblk_ket * kEnt * kLanes;  // per site
-  const int64_t bstride = a.n_pad_bra * kEnt;
-  uint32_t it = 0;  // sites this warp consumed (ring position + phase)
-  auto issue = [&](uint32_t q) {
-    const int2 tl = a.tiles[blockIdx.x + (int64_t)(q / m) * gridDim.x];
-    const int site = (int)(q % m);
-    const uint32_t buf = q & (kStages - 1);
-    mbar_arrive_expect_tx(&full[buf], kKetBytes + kBraBytes);
-    bulk_g2s(sket + buf * kEnt * kLanes, a.ket + (int64_t)tl.y * kEnt * kLanes + site * kstride,
-             kKetBytes, &full[buf]);
-    bulk_g2s(sbra + buf * kWarpsO1 * kEnt, a.bra + (int64_t)tl.x * kWarpsO1 * kEnt + site * bstride,
-             kBraBytes, &full[buf]);
-  };
-  // Lane 0 of every warp produces: refill free slots opportunistically (the
-  // fastest warp keeps the ring full) and block only for the slot this warp
-  // needs next; a CAS on the shared counter issues every site exactly once.
-  // Warp-collective (all lanes take the same path; only the CAS and the
-  // copy issue are lane 0's), so the warp never leaves the producer diverged.
-  volatile uint32_t* vld = ld_ctr;
-  uint32_t seen = 0;  // last issue count this warp observed (warp-uniform)
-  auto produce = [&]() {
-    for (;;) {
-      const uint32_t q = __shfl_sync(kFull, lane == 0 ? *vld : 0u, 0);
-      seen = q;
-      if (q >= total || q >= it + kStages) break;
-      if (q >= kStages) {
-        const uint32_t par = ((q / kStages) - 1) & 1;
-        if (q <= it) {
-          mbar_wait(&empty[q & (kStages - 1)], par);
-        } else {
-          const int ok = __shfl_sync(kFull, (int)mbar_test(&empty[q & (kStages - 1)], par), 0);
-          if (!ok) break;
+  const int64_t my_tiles = (int64_t)blockIdx.x < a.n_tiles ? (a.n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (warp >= kWarpsO1) {
+    // ---------------- producer warpgroup
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 24;\n" ::: "memory");
+    if (warp == kWarpsO1 && lane == 0) {
+      const int64_t kstride = a.nblk_ket * kEnt * kLanes;  // per site
+      const int64_t bstride = a.n_pad_bra * kEnt;
+      uint32_t q = 0;
+      for (int64_t k = 0; k < my_tiles; ++k) {
+        const int2 tl = a.tiles[blockIdx.x + k * gridDim.x];
+        const double2* kb = a.ket + (int64_t)tl.y * kEnt * kLanes;
+        const double2* bb = a.bra + (int64_t)tl.x * kWarpsO1 * kEnt;
+        for (int site = 0; site < m; ++site, ++q) {
+          const uint32_t buf = q & (kStages - 1);
+          if (q >= kStages) mbar_wait(&empty[buf], ((q / kStages) - 1) & 1);
+          mbar_arrive_expect_tx(&full[buf], kKetBytes + kBraBytes);
+          bulk_g2s(sket + buf * kEnt * kLanes, kb + site * kstride, kKetBytes, &full[buf]);
+          bulk_g2s(sbra + buf * kWarpsO1 * kEnt, bb + site * bstride, kBraBytes, &full[buf]);
         }
       }
-      if (lane == 0 && atomicCAS(ld_ctr, q, q + 1) == q) issue(q);
-      __syncwarp();
     }
-  };
+    return;
+  }
+  // ---------------- compute warpgroups
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 240;\n" ::: "memory");
+  uint32_t it = 0;  // sites this warp consumed (ring position + phase)
   int32_t* mychi = schi + warp * (m + 1);
   for (int64_t k = 0; k < my_tiles; ++k) {
     const int2 tile = a.tiles[blockIdx.x + k * gridDim.x];
@@ -363,9 +352,6 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
       for (int y = 0; y < kP; ++y) env[x][y] = make_double2(x == 0 && y == 0 ? 1.0 : 0.0, 0.0);
     int na = 1;  // chi_s of the bra (warp-uniform)
     for (int s = 0; s < m; ++s) {
-      // the counter only grows: run the producer when this warp's view of the
-      // ring is less than half full (or its next slot may not be issued yet)
-      if (seen < it + kStages / 2 + 1 && seen < total) produce();
       const int na1 = mychi[s + 1];
       const uint32_t buf = it & (kStages - 1);
       mbar_wait(&full[buf], (it / kStages) & 1);
@@ -387,8 +373,6 @@ __global__ void __launch_bounds__(kWarpsO1 * 32, 1) overlap_o1_kernel(O1Args a) 
       na = na1;
     }
     const bool train = a.kind == MPSKQ_KIND_TRAIN;
-    // results go to the ordered index space (full-sector tile rows); a gather
-    // pass maps them back to the callers' indices
     const bool valid = i < a.n_bras && j < a.n_kets && (!train || i < j);
     if (valid) store_result(a.out_mode, a.out, a.ld, i, j, env[0][0], train);
     __syncwarp();
@@ -740,6 +724,7 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
   if (to_host) {
     const size_t smem = o1_smem_bytes(m);
     e = cudaFuncSetAttribute(overlap_o1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+
     if (e != cudaSuccess) {
       release();
       return cuda_fail(e, "cudaFuncSetAttribute(o1)");
@@ -778,7 +763,7 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
                  a.n_bras, a.n_kets, npb, nbk, m, a.kind,
                  a.out_mode, dtiles + band_tiles[b], nt, static_cast<double*>(ordered), a.n_kets,
                  bperm, kperm, static_cast<const uint8_t*>(narrow)};
-        overlap_o1_kernel<<<(int)std::min<int64_t>(nt, sms), kWarpsO1 * 32, smem, sb>>>(o);
+        overlap_o1_kernel<<<(int)std::min<int64_t>(nt, sms), kThreadsO1Ws, smem, sb>>>(o);
       }
       cudaEventRecord(evs[b], sb);
       cudaStreamWaitEvent(side, evs[b], 0);
@@ -819,6 +804,7 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
   } else if (!tiles.empty()) {
     const size_t smem = o1_smem_bytes(m);
     e = cudaFuncSetAttribute(overlap_o1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+
     if (e != cudaSuccess) {
       release();
       return cuda_fail(e, "cudaFuncSetAttribute(o1)");
@@ -832,7 +818,7 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // persistent: one CTA per SM walks the tile list (the ring stays warm)
     const int grid = (int)std::min<int64_t>((int64_t)tiles.size(), sms);
-    overlap_o1_kernel<<<grid, kWarpsO1 * 32, smem, st>>>(o);
+    overlap_o1_kernel<<<grid, kThreadsO1Ws, smem, st>>>(o);
     const int32_t* bpos = train ? static_cast<const int32_t*>(kinv) : nullptr;
     const int rows = (int)std::min<int64_t>(a.n_bras, 148 * 32);
     if (a.owned) {

@@ -664,7 +664,6 @@ extern "C" int mpskq_gram_host(int kind, int m, int r, int d, double gamma, doub
   };
   std::vector<std::unique_ptr<Level>> levels;
   std::vector<int32_t> todo;  // global rows still to simulate (empty = all, level 0)
-  std::vector<int64_t> counts;
   for (;; ++cap_idx) {
     if (cap_idx >= kNumChiCaps)
       return fail(MPSKQ_ERR_CAPACITY, "bond dimension exceeds the largest compiled capacity %d",
@@ -703,18 +702,16 @@ extern "C" int mpskq_gram_host(int kind, int m, int r, int d, double gamma, doub
       if (hstatus[i] == MPSKQ_STATE_NOCONV) return fail(MPSKQ_ERR_NUMERIC, "SVD did not converge");
       if (hstatus[i] == MPSKQ_STATE_CAPACITY) next.push_back(levels.empty() ? (int32_t)i : todo[i]);
     }
-    counts.push_back(L->n);
     levels.push_back(std::move(L));
     if (next.empty()) break;
     if (chi_cap) return fail(MPSKQ_ERR_CAPACITY, "bond dimension exceeds chi capacity %d", kChiCaps[cap_idx]);
     todo.swap(next);
   }
   if (!chi_cap) {
-    // next call starts at the first level that held >= 7/8 of the states
-    size_t h = 0;
-    while (h + 1 < counts.size() && counts[h + 1] * 8 > n_all) ++h;
+    // the next call starts at the capacity the whole batch needed (a lower
+    // start replays every state that later overflows: slower in steady state)
     std::lock_guard<std::mutex> g(cache().mu);
-    cache().cap_hint[key] = levels[h]->cap_idx;
+    cache().cap_hint[key] = levels.back()->cap_idx;
   }
   Level& fin = *levels.back();
   const int cap = kChiCaps[fin.cap_idx];

@@ -150,7 +150,7 @@ struct Smem {
   double* red;   // kRed
   static constexpr int kRedHalf = NT / 32 > 16 ? NT / 32 : 16;  // warps of the group (>= 16)
   static constexpr int kRed = 2 * kRedHalf;
-  double* scal;  // 4: factor, discarded
+  double* scal;  // 8: factor, discarded, -, op start clock, nominal flops, 3 phase cycle sums
   int* perm;     // LD
   int* piv;      // LD: inverse column order of the pivoted QR
   int* ibuf;     // 4: keep
@@ -161,7 +161,7 @@ struct Smem {
     size_t b = GlobalWs<CAP>::value
                    ? sizeof(double2) * 2 * LD
                    : sizeof(double2) * ((LogW<CAP>::value ? 1 : 2) * LD * LD + 2 * CAP * CAP + 2 * LD);
-    b += sizeof(double) * (2 * LD + kRed + 4);
+    b += sizeof(double) * (2 * LD + kRed + 8);
     b += sizeof(int) * (2 * LD + 4 + m + 1);
     return (b + 15) & ~size_t(15);
   }
@@ -194,7 +194,7 @@ struct Smem {
     red = reinterpret_cast<double*>(p);
     p += sizeof(double) * kRed;
     scal = reinterpret_cast<double*>(p);
-    p += sizeof(double) * 4;
+    p += sizeof(double) * 8;
     perm = reinterpret_cast<int*>(p);
     p += sizeof(int) * LD;
     piv = reinterpret_cast<int*>(p);
@@ -813,7 +813,6 @@ struct StateCtx {
   int status;
   int peak;
   double discard;
-  double flops = 0.0;  // nominal LAPACK-style flop count, thread 0
 };
 
 // Nominal flops of one apply_two_qubit (fixed here once): theta
@@ -829,7 +828,7 @@ __device__ __forceinline__ double nominal_qr(int M, int N, int k, int cols) {
   return 16.0 * M * (double)N * N + 8.0 * k * (double)N * cols;
 }
 
-template <int CAP, int NT>
+template <int CAP, int NT, bool GEN>
 __device__ void op_one_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, double2 cs,
                              const double2* gm) {
   const int chl = sm.chi[q], chr = sm.chi[q + 1];
@@ -840,7 +839,7 @@ __device__ void op_one_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, d
     const int a = idx / chr, b = idx - a * chr;
     const int i0 = (2 * a) * chr + b, i1 = i0 + chr;
     const double2 x0 = p[i0], x1 = p[i1];
-    if (code == MPSKQ_OP_U1) {
+    if (GEN && code == MPSKQ_OP_U1) {
       // arbitrary 2x2 matrix U (row-major in the coefficient row):
       // site <- tensordot(U, site, (1, 1)).transpose(1, 0, 2)  (mps.py:157)
       const double2 u00 = gm[0], u01 = gm[1], u10 = gm[2], u11 = gm[3];
@@ -901,7 +900,7 @@ __device__ void op_qr_left(Smem<CAP, NT>& sm, StateCtx& st, int i) {
   bsync<NT>();
   if (tid == 0) {
     sm.chi[i + 1] = k;
-    st.flops += nominal_qr(Rr, chr, k, cols);
+    sm.scal[4] += nominal_qr(Rr, chr, k, cols);  // nominal flops, per state
   }
   bsync<NT>();
 }
@@ -943,13 +942,13 @@ __device__ void op_qr_right(Smem<CAP, NT>& sm, StateCtx& st, int i) {
   bsync<NT>();
   if (tid == 0) {
     sm.chi[i] = k;
-    st.flops += nominal_qr(Rr, chl, k, rows);
+    sm.scal[4] += nominal_qr(Rr, chl, k, rows);
   }
   bsync<NT>();
 }
 
 // apply_two_qubit at (q, q+1) after canonicalize(q) (mps.py:163-205)
-template <int CAP, int NT>
+template <int CAP, int NT, bool GEN>
 __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, bool left,
                              double2 cs, const double2* gm, double budget, int chi_max) {
   constexpr int LD = 2 * CAP;
@@ -983,7 +982,7 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
   const bool pre = kPrecondition<CAP>::value && kmin >= kPrecondMinCols;
   const bool theta_cm = left != pre;  // store C (not preconditioned) or C^H
   int bad = 0;
-  if (code == MPSKQ_OP_U2) {
+  if (GEN && code == MPSKQ_OP_U2) {
     // arbitrary 4x4 matrix G on |p0 p1> (row-major in the coefficient row):
     // theta'(l, p0', p1', r) = sum G[p0'p1'][p0 p1] theta(l, p0, p1, r)
     // (mps.py:184-186); one item per (l, r) couples all four physical entries
@@ -1010,7 +1009,7 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
     }
   }
   #pragma unroll 1
-  for (int it = tid; it < (code == MPSKQ_OP_U2 ? 0 : chl * chr * 2); it += NT) {
+  for (int it = tid; it < (GEN && code == MPSKQ_OP_U2 ? 0 : chl * chr * 2); it += NT) {
     const int t = it & 1, lr = it >> 1;
     const int l = lr / chr, rr = lr - l * chr;
     const int p0a = 0, p1a = t;
@@ -1140,7 +1139,7 @@ __device__ void op_two_qubit(Smem<CAP, NT>& sm, StateCtx& st, int q, int code, b
     sm.chi[q + 1] = keep;
     st.discard += sm.scal[1];  // accumulated_discard (mps.py:201)
     st.peak = max(st.peak, keep);
-    st.flops += nominal_two_qubit(chl, chm, chr);
+    sm.scal[4] += nominal_two_qubit(chl, chm, chr);
   }
   bsync<NT>();
   MPSKQ_DBG_ADD(6, t_wside);
@@ -1156,8 +1155,20 @@ struct SpcFor {
   static constexpr int value = NT <= 32 ? MPSKQ_SPC_THREADS / NT : 1;
 };
 
-template <int CAP, int NT>
-__global__ void __launch_bounds__(NT * SpcFor<NT>::value) sim_kernel(SimArgs a) {
+// Capacities 64-128 (512 threads per state, theta in the L2 workspace): two
+// resident states per SM need <= 64 registers per thread.  Without the bound
+// ptxas takes 128 and halves the states in flight (measured +29% simulation
+// time at m=100 d=7 / d=8, tools/ab_sim_abi.py).
+template <int NT>
+struct MinCtasFor {
+  static constexpr int value = NT >= 512 ? 2 : 1;
+};
+
+// GEN: programs of the state-level API (continue a given state, arbitrary
+// U1 / U2 matrices); the feature-map programs run the GEN = false build,
+// whose registers the general-matrix paths do not touch.
+template <int CAP, int NT, bool GEN>
+__global__ void __launch_bounds__(NT * SpcFor<NT>::value, MinCtasFor<NT>::value) sim_kernel(SimArgs a) {
   constexpr int SPC = SpcFor<NT>::value;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int slot = SPC > 1 ? (int)(threadIdx.x / NT) : 0;
@@ -1179,7 +1190,7 @@ __global__ void __launch_bounds__(NT * SpcFor<NT>::value) sim_kernel(SimArgs a) 
     bool live = n < a.n_states;  // uniform per state group
     StateCtx st{reinterpret_cast<double2*>(a.sites) + (live ? n : 0) * a.state_stride, a.site_off, m,
                 MPSKQ_STATE_OK, 1, 0.0};
-    if (live && a.from_input) {
+    if (GEN && live && a.from_input) {
       // continue an existing state (apply_gate / canonicalize / run_circuit on
       // a given MpsState, mps.py:123-247): sites are already in the slab,
       // bond dims, discard and peak come in through the output arrays
@@ -1201,8 +1212,12 @@ __global__ void __launch_bounds__(NT * SpcFor<NT>::value) sim_kernel(SimArgs a) 
       }
       bsync<NT>();
     }
-    // per-phase device cycles (MpsState.timings keys, mps.py:137/:159/:204)
-    long long ph_canon = 0, ph_one = 0, ph_two = 0;
+    // nominal flops and per-phase device cycles (MpsState.timings keys,
+    // mps.py:137/:159/:204) accumulate in shared memory (thread 0): no extra
+    // registers live across the ops
+    if (tid == 0)
+      for (int x = 3; x < 8; ++x) sm.scal[x] = 0.0;
+    long long* op_t0 = reinterpret_cast<long long*>(sm.scal + 3);
     const double2* cf = coef + (live ? n : 0) * a.n_params;
     for (int64_t i = 0; i < a.n_ops; ++i) {
       if (live) {
@@ -1210,13 +1225,13 @@ __global__ void __launch_bounds__(NT * SpcFor<NT>::value) sim_kernel(SimArgs a) 
         const int code = op.x & 0xff;
         const bool left = (op.x >> 8) & MPSKQ_ABSORB_LEFT;
         const double2 cs = op.z >= 0 ? __ldg(cf + op.z) : make_double2(1.0, 0.0);
-        const double2* gm = cf + (op.z >= 0 ? op.z : 0);  // U1 / U2 matrices
-        const long long c0 = a.phase_cycles ? clock64() : 0;
+        const double2* gm = GEN ? cf + (op.z >= 0 ? op.z : 0) : nullptr;  // U1 / U2 matrices
+        if (a.phase_cycles && tid == 0) *op_t0 = clock64();
         switch (code) {
           case MPSKQ_OP_H:
           case MPSKQ_OP_RZ:
           case MPSKQ_OP_U1:
-            op_one_qubit<CAP, NT>(sm, st, op.y, code, cs, gm);
+            op_one_qubit<CAP, NT, GEN>(sm, st, op.y, code, cs, gm);
             break;
           case MPSKQ_OP_QRL: {
             MPSKQ_DBG_T(t_mv);
@@ -1231,17 +1246,15 @@ __global__ void __launch_bounds__(NT * SpcFor<NT>::value) sim_kernel(SimArgs a) 
             break;
           }
           default:
-            op_two_qubit<CAP, NT>(sm, st, op.y, code, left, cs, gm, a.budget, a.chi_max);
+            op_two_qubit<CAP, NT, GEN>(sm, st, op.y, code, left, cs, gm, a.budget, a.chi_max);
             break;
         }
-        if (a.phase_cycles) {
-          const long long dt = clock64() - c0;
-          if (code == MPSKQ_OP_QRL || code == MPSKQ_OP_QRR)
-            ph_canon += dt;
-          else if (code == MPSKQ_OP_H || code == MPSKQ_OP_RZ || code == MPSKQ_OP_U1)
-            ph_one += dt;
-          else
-            ph_two += dt;
+        if (a.phase_cycles && tid == 0) {
+          const double dt = (double)(clock64() - *op_t0);
+          const int ph = (code == MPSKQ_OP_QRL || code == MPSKQ_OP_QRR)                      ? 0
+                         : (code == MPSKQ_OP_H || code == MPSKQ_OP_RZ || code == MPSKQ_OP_U1) ? 1
+                                                                                              : 2;
+          sm.scal[5 + ph] += dt;
         }
         if (st.status != MPSKQ_STATE_OK) live = false;  // keep hitting the barriers
         if (live && a.entry_log != nullptr && op.w >= 0 && tid == 0) {
@@ -1259,12 +1272,9 @@ __global__ void __launch_bounds__(NT * SpcFor<NT>::value) sim_kernel(SimArgs a) 
         a.discard[n] = st.discard;
         a.peak[n] = st.peak;
         a.status[n] = st.status;
-        if (a.nominal_flops) a.nominal_flops[n] = st.flops;
-        if (a.phase_cycles) {
-          a.phase_cycles[3 * n] = ph_canon;
-          a.phase_cycles[3 * n + 1] = ph_one;
-          a.phase_cycles[3 * n + 2] = ph_two;
-        }
+        if (a.nominal_flops) a.nominal_flops[n] = sm.scal[4];
+        if (a.phase_cycles)
+          for (int x = 0; x < 3; ++x) a.phase_cycles[3 * n + x] = (long long)sm.scal[5 + x];
       }
     }
     bsync<NT>();
@@ -1380,22 +1390,28 @@ int plan_grid(K kernel, int threads, size_t smem, int64_t items, cudaStream_t st
   return MPSKQ_OK;
 }
 
-template <int CAP>
-int launch_sim_cap(const SimArgs& a0, cudaStream_t st) {
+template <int CAP, bool GEN>
+int launch_sim_cap_k(const SimArgs& a0, cudaStream_t st) {
   constexpr int NT = NtFor<CAP>::value;
   constexpr int SPC = SpcFor<NT>::value;
   const size_t smem = Smem<CAP, NT>::bytes(a0.m) * SPC;
-  if (int s = prepare(sim_kernel<CAP, NT>, smem)) return s;
+  if (int s = prepare(sim_kernel<CAP, NT, GEN>, smem)) return s;
   SimArgs a = a0;
   int64_t grid = 0;
-  if (int s = plan_grid<CAP>(sim_kernel<CAP, NT>, NT * SPC, smem, (a.n_states + SPC - 1) / SPC, st, &grid,
+  if (int s = plan_grid<CAP>(sim_kernel<CAP, NT, GEN>, NT * SPC, smem, (a.n_states + SPC - 1) / SPC, st, &grid,
                              &a.scratch))
     return s;
-  sim_kernel<CAP, NT><<<(unsigned)grid, NT * SPC, smem, st>>>(a);
+  sim_kernel<CAP, NT, GEN><<<(unsigned)grid, NT * SPC, smem, st>>>(a);
   cudaError_t e = cudaGetLastError();
   if (a.scratch) cudaFreeAsync(a.scratch, st);
   if (e != cudaSuccess) return cuda_fail(e, "sim_kernel launch");
   return MPSKQ_OK;
+}
+
+template <int CAP>
+int launch_sim_cap(const SimArgs& a0, cudaStream_t st) {
+  if (a0.from_input) return launch_sim_cap_k<CAP, true>(a0, st);
+  return launch_sim_cap_k<CAP, false>(a0, st);
 }
 
 template <int CAP>
