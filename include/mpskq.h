@@ -181,12 +181,13 @@ int mpskq_relayout(int m, int64_t n, const double* src_sites_dev, const int64_t*
  * site tensors back to back ((chi_l, 2, chi_r) row-major, the MPS1 payload
  * order, mps.py:294-314) from complex offset state_off_dev[i]; the caller
  * computes state_off as the prefix sum of sum_s 2 chi_s chi_{s+1}.  Unpack
- * is the inverse into a batch layout.                                     */
+ * is the inverse into a batch layout (optionally into rows dst_rows; the
+ * per-state capacity escalation keeps finished levels packed this way).    */
 int mpskq_pack_exact(int m, int64_t n, const double* sites_dev, const int64_t* site_off_dev, int64_t state_stride,
                      const int32_t* chi_dev, const int64_t* state_off_dev, double* packed_dev, void* stream);
 int mpskq_unpack_exact(int m, int64_t n, const double* packed_dev, const int64_t* state_off_dev,
                        const int32_t* chi_dev, double* sites_dev, const int64_t* site_off_dev, int64_t state_stride,
-                       void* stream);
+                       const int32_t* dst_rows_dev /* nullable: state i -> layout row dst_rows[i] */, void* stream);
 
 /* ---------------------------------------------------------------- truncated SVD
  * svd_truncated (tensor.py:87-123) on a batch of rows x cols complex

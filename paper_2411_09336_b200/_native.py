@@ -81,7 +81,7 @@ _SIGNATURES = {
          C.c_int64, C.c_int, C.c_int, _vp, C.c_int64, _vp],
     ),
     "mpskq_pack_exact": (C.c_int, [C.c_int, C.c_int64, _vp, _vp, C.c_int64, _vp, _vp, _vp, _vp]),
-    "mpskq_unpack_exact": (C.c_int, [C.c_int, C.c_int64, _vp, _vp, _vp, _vp, _vp, C.c_int64, _vp]),
+    "mpskq_unpack_exact": (C.c_int, [C.c_int, C.c_int64, _vp, _vp, _vp, _vp, _vp, C.c_int64, _vp, _vp]),
     "mpskq_owned_rows": (C.c_int, [C.c_int, C.c_int64, C.c_int, C.c_int, _i64p]),
     "mpskq_overlap_owned_rows": (
         C.c_int,

@@ -116,7 +116,7 @@ int launch_copy_rows(const void* src, void* dst, int64_t row_bytes, int64_t n, c
                      const int32_t* dst_idx, void* stream);
 
 int launch_pack_exact(int m, int64_t n, double* sites, const int64_t* site_off, int64_t stride, const int32_t* chi,
-                      const int64_t* state_off, double* packed, int unpack, void* stream);
+                      const int64_t* state_off, double* packed, int unpack, const int32_t* rows, void* stream);
 
 int launch_encode(const double* X, int64_t n_rows, int m, int r, int d, double gamma, double* coef,
                   int* bad, void* stream);

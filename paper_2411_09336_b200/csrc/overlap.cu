@@ -291,6 +291,12 @@ struct O1Args {
 // every compute warp could refill slots through a CAS on a shared counter,
 // ran 147.8 ms at N=6400 against 142 ms for this one, `profiles/r02_ab_o1_ws.txt`.)
 constexpr int kThreadsO1Ws = (kWarpsO1 + 4) * 32;
+#ifndef MPSKQ_O1_CN
+#define MPSKQ_O1_CN 0  // A/B knob: bra bonds + ket-block narrow flags in one shared table
+#endif
+#ifndef MPSKQ_O1_PSLEEP
+#define MPSKQ_O1_PSLEEP 0  // A/B knob: producer polls the empty barriers with this nanosleep (0: try_wait)
+#endif
 
 __global__ void __launch_bounds__(kThreadsO1Ws, 1) overlap_o1_kernel(O1Args a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -323,7 +329,15 @@ __global__ void __launch_bounds__(kThreadsO1Ws, 1) overlap_o1_kernel(O1Args a) {
         const double2* bb = a.bra + (int64_t)tl.x * kWarpsO1 * kEnt;
         for (int site = 0; site < m; ++site, ++q) {
           const uint32_t buf = q & (kStages - 1);
-          if (q >= kStages) mbar_wait(&empty[buf], ((q / kStages) - 1) & 1);
+          if (q >= kStages) {
+#if MPSKQ_O1_PSLEEP
+            // poll politely: the producer shares an SM sub-partition with two
+            // compute warps, and a freed slot has kStages - 1 sites of slack
+            while (!mbar_test(&empty[buf], ((q / kStages) - 1) & 1)) __nanosleep(MPSKQ_O1_PSLEEP);
+#else
+            mbar_wait(&empty[buf], ((q / kStages) - 1) & 1);
+#endif
+          }
           mbar_arrive_expect_tx(&full[buf], kKetBytes + kBraBytes);
           bulk_g2s(sket + buf * kEnt * kLanes, kb + site * kstride, kKetBytes, &full[buf]);
           bulk_g2s(sbra + buf * kWarpsO1 * kEnt, bb + site * bstride, kBraBytes, &full[buf]);
@@ -343,7 +357,14 @@ __global__ void __launch_bounds__(kThreadsO1Ws, 1) overlap_o1_kernel(O1Args a) {
     const int64_t ic = i < a.n_bras ? i : a.n_bras - 1;
     const int64_t ib = a.bperm ? a.bperm[ic] : ic;  // bra index of this warp
     const uint8_t* narrow = a.kb_narrow + (int64_t)tile.y * (m + 1);
+#if MPSKQ_O1_CN
+    // bra bond in the low byte, the ket block's narrow flag in bit 8: one
+    // shared load per site instead of a shared and two global loads
+    for (int b = lane; b <= m; b += kLanes)
+      mychi[b] = __ldg(a.bra_chi + ib * (m + 1) + b) | ((int32_t)__ldg(narrow + b) << 8);
+#else
     for (int b = lane; b <= m; b += kLanes) mychi[b] = __ldg(a.bra_chi + ib * (m + 1) + b);
+#endif
     __syncwarp();
     double2 env[kP][kP];
 #pragma unroll
@@ -351,13 +372,22 @@ __global__ void __launch_bounds__(kThreadsO1Ws, 1) overlap_o1_kernel(O1Args a) {
 #pragma unroll
       for (int y = 0; y < kP; ++y) env[x][y] = make_double2(x == 0 && y == 0 ? 1.0 : 0.0, 0.0);
     int na = 1;  // chi_s of the bra (warp-uniform)
+#if MPSKQ_O1_CN
+    bool nar_l = (mychi[0] >> 8) != 0;
+#endif
     for (int s = 0; s < m; ++s) {
+#if MPSKQ_O1_CN
+      const int cn1 = mychi[s + 1];
+      const int na1 = cn1 & 0xff;
+      const bool nar_r = (cn1 >> 8) != 0;
+#else
       const int na1 = mychi[s + 1];
+      const bool nar_l = __ldg(narrow + s) != 0, nar_r = __ldg(narrow + s + 1) != 0;
+#endif
       const uint32_t buf = it & (kStages - 1);
       mbar_wait(&full[buf], (it / kStages) & 1);
       const double2* B = sket + buf * kEnt * kLanes + lane;  // B[e] at B[e * 32]
       const double2* A = sbra + buf * kWarpsO1 * kEnt + warp * kEnt;
-      const bool nar_l = __ldg(narrow + s) != 0, nar_r = __ldg(narrow + s + 1) != 0;
       double2 T[kP][2][kP];
       using namespace o1;
       switch (na) {
@@ -371,6 +401,9 @@ __global__ void __launch_bounds__(kThreadsO1Ws, 1) overlap_o1_kernel(O1Args a) {
       if (lane == 0) mbar_arrive(&empty[buf]);
       ++it;
       na = na1;
+#if MPSKQ_O1_CN
+      nar_l = nar_r;
+#endif
     }
     const bool train = a.kind == MPSKQ_KIND_TRAIN;
     const bool valid = i < a.n_bras && j < a.n_kets && (!train || i < j);

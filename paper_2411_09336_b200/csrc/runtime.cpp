@@ -384,15 +384,15 @@ int mpskq_pack_exact(int m, int64_t n, const double* sites_dev, const int64_t* s
                      const int32_t* chi_dev, const int64_t* state_off_dev, double* packed_dev, void* stream) {
   if (m < 1 || n < 0) return fail(MPSKQ_ERR_INVALID, "bad pack sizes");
   return launch_pack_exact(m, n, const_cast<double*>(sites_dev), site_off_dev, state_stride, chi_dev, state_off_dev,
-                           packed_dev, 0, stream);
+                           packed_dev, 0, nullptr, stream);
 }
 
 int mpskq_unpack_exact(int m, int64_t n, const double* packed_dev, const int64_t* state_off_dev,
                        const int32_t* chi_dev, double* sites_dev, const int64_t* site_off_dev, int64_t state_stride,
-                       void* stream) {
+                       const int32_t* dst_rows_dev, void* stream) {
   if (m < 1 || n < 0) return fail(MPSKQ_ERR_INVALID, "bad unpack sizes");
   return launch_pack_exact(m, n, sites_dev, site_off_dev, state_stride, chi_dev, state_off_dev,
-                           const_cast<double*>(packed_dev), 1, stream);
+                           const_cast<double*>(packed_dev), 1, dst_rows_dev, stream);
 }
 
 int mpskq_svd_truncated_batched(int rows, int cols, int64_t batch, const double* mats_dev,
@@ -660,7 +660,7 @@ extern "C" int mpskq_gram_host(int kind, int m, int r, int d, double gamma, doub
   struct Level {
     int cap_idx = 0;
     int64_t n = 0, stride = 0;
-    AsyncBuf sites, chi, disc, peak, status, doff, rows, coef;
+    AsyncBuf sites, chi, disc, peak, status, doff, rows, coef, packed, soff;  // packed: finished, exact
   };
   std::vector<std::unique_ptr<Level>> levels;
   std::vector<int32_t> todo;  // global rows still to simulate (empty = all, level 0)
@@ -702,6 +702,26 @@ extern "C" int mpskq_gram_host(int kind, int m, int r, int d, double gamma, doub
       if (hstatus[i] == MPSKQ_STATE_NOCONV) return fail(MPSKQ_ERR_NUMERIC, "SVD did not converge");
       if (hstatus[i] == MPSKQ_STATE_CAPACITY) next.push_back(levels.empty() ? (int32_t)i : todo[i]);
     }
+    if (!next.empty() && !chi_cap) {
+      // keep this level's states exactly packed (their own bond dims) until
+      // the final capacity is known; the padded level buffer is released
+      std::vector<int32_t> hchi((m + 1) * L->n);
+      CK(cudaMemcpyAsync(hchi.data(), L->chi.p, sizeof(int32_t) * hchi.size(), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      std::vector<int64_t> hoff(L->n);
+      int64_t tot = 0;
+      for (int64_t i = 0; i < L->n; ++i) {
+        hoff[i] = tot;
+        for (int b = 0; b < m; ++b) tot += 2 * (int64_t)hchi[i * (m + 1) + b] * hchi[i * (m + 1) + b + 1];
+      }
+      ST(L->soff.alloc(sizeof(int64_t) * L->n, st));
+      CK(cudaMemcpyAsync(L->soff.p, hoff.data(), sizeof(int64_t) * L->n, cudaMemcpyHostToDevice, st));
+      ST(L->packed.alloc(sizeof(double) * 2 * std::max<int64_t>(tot, 1), st));
+      ST(launch_pack_exact(m, L->n, L->sites.as<double>(), L->doff.as<int64_t>(), L->stride, L->chi.as<int32_t>(),
+                           L->soff.as<int64_t>(), L->packed.as<double>(), 0, nullptr, st));
+      CK(cudaStreamSynchronize(st));  // hoff / hchi leave scope
+      L->sites.reset();
+    }
     levels.push_back(std::move(L));
     if (next.empty()) break;
     if (chi_cap) return fail(MPSKQ_ERR_CAPACITY, "bond dimension exceeds chi capacity %d", kChiCaps[cap_idx]);
@@ -732,8 +752,12 @@ extern "C" int mpskq_gram_host(int kind, int m, int r, int d, double gamma, doub
     for (auto& Lp : levels) {  // later levels overwrite the rows that overflowed earlier ones
       Level& L = *Lp;
       const int32_t* rows = L.rows.p ? L.rows.as<int32_t>() : nullptr;
-      ST(launch_relayout(m, L.n, L.sites.as<double>(), L.doff.p ? L.doff.as<int64_t>() : doff.as<int64_t>(),
-                         L.stride, L.chi.as<int32_t>(), sites.as<double>(), doff.as<int64_t>(), stride, rows, st));
+      if (L.packed.p)
+        ST(launch_pack_exact(m, L.n, sites.as<double>(), doff.as<int64_t>(), stride, L.chi.as<int32_t>(),
+                             L.soff.as<int64_t>(), L.packed.as<double>(), 1, rows, st));
+      else
+        ST(launch_relayout(m, L.n, L.sites.as<double>(), L.doff.p ? L.doff.as<int64_t>() : doff.as<int64_t>(),
+                           L.stride, L.chi.as<int32_t>(), sites.as<double>(), doff.as<int64_t>(), stride, rows, st));
       ST(launch_copy_rows(L.chi.p, chi.p, sizeof(int32_t) * (m + 1), L.n, nullptr, rows, st));
       ST(launch_copy_rows(L.disc.p, disc.p, sizeof(double), L.n, nullptr, rows, st));
       ST(launch_copy_rows(L.peak.p, peak.p, sizeof(int32_t), L.n, nullptr, rows, st));

@@ -1508,10 +1508,11 @@ int launch_relayout(int m, int64_t n, const double* src, const int64_t* src_off,
 // unpack = 0: layout -> packed; 1: packed -> layout.
 __global__ void pack_exact_kernel(int m, int64_t n, double2* __restrict__ sites, const int64_t* __restrict__ site_off,
                                   int64_t stride, const int32_t* __restrict__ chi,
-                                  const int64_t* __restrict__ state_off, double2* __restrict__ packed, int unpack) {
+                                  const int64_t* __restrict__ state_off, double2* __restrict__ packed, int unpack,
+                                  const int32_t* __restrict__ rows) {
   for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
     const int32_t* c = chi + i * (m + 1);
-    double2* lay = sites + i * stride;
+    double2* lay = sites + (int64_t)(rows ? rows[i] : i) * stride;  // layout row (unpack: destination)
     double2* pk = packed + state_off[i];
     int64_t o = 0;
     for (int s = 0; s < m; ++s) {
@@ -1527,11 +1528,11 @@ __global__ void pack_exact_kernel(int m, int64_t n, double2* __restrict__ sites,
 }
 
 int launch_pack_exact(int m, int64_t n, double* sites, const int64_t* site_off, int64_t stride, const int32_t* chi,
-                      const int64_t* state_off, double* packed, int unpack, void* stream) {
+                      const int64_t* state_off, double* packed, int unpack, const int32_t* rows, void* stream) {
   if (n <= 0) return MPSKQ_OK;
   pack_exact_kernel<<<(unsigned)std::min<int64_t>(n, 148 * 16), 128, 0, static_cast<cudaStream_t>(stream)>>>(
       m, n, reinterpret_cast<double2*>(sites), site_off, stride, chi, state_off, reinterpret_cast<double2*>(packed),
-      unpack);
+      unpack, rows);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "pack_exact launch");
   return MPSKQ_OK;

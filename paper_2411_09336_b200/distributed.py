@@ -100,7 +100,7 @@ def _unpack_native(packed, off, chi, m, stride, site_off_dev):
 
     sites = packed.new_empty((chi.shape[0], 2 * stride))
     N.check(N.lib().mpskq_unpack_exact(m, chi.shape[0], dptr(packed), dptr(off), dptr(chi), dptr(sites),
-                                       dptr(site_off_dev), stride, stream_ptr()))
+                                       dptr(site_off_dev), stride, None, stream_ptr()))
     return sites
 
 

@@ -435,6 +435,15 @@ def simulate_program(prog: Program, coef, budget: float, chi_max: int = 0,
             break
         if chi_cap is not None:
             raise RuntimeError(f"bond dimension exceeds the largest usable chi capacity {order[-1]}")
+        # keep this level's states exactly packed (their own bond dims, no
+        # capacity padding) until the final layout is known: at large
+        # capacities the padded levels would otherwise stack up in HBM
+        ent = (2 * lv["chi"][:, :-1].long() * lv["chi"][:, 1:].long()).sum(1)
+        lv["state_off"] = torch.cumsum(ent, 0) - ent
+        lv["packed"] = torch.empty(max(2 * int(ent.sum().item()), 2), dtype=torch.float64, device=dev)
+        N.check(N.lib().mpskq_pack_exact(m, nl, dptr(lv["sites"]), dptr(off_d), stride, dptr(lv["chi"]),
+                                         dptr(lv["state_off"]), dptr(lv["packed"]), stream_ptr()))
+        lv["sites"] = None
         ov = torch.from_numpy(over).to(dev)
         rows = ov if rows is None else rows.index_select(0, ov)
     else:
@@ -459,9 +468,15 @@ def simulate_program(prog: Program, coef, budget: float, chi_max: int = 0,
         elog = torch.empty((n, prog.n_gates), dtype=torch.int64, device=dev) if memory_log else None
         for lv in levels:  # later levels overwrite the rows that overflowed earlier ones
             r32 = None if lv["rows"] is None else lv["rows"].to(torch.int32)
-            N.check(N.lib().mpskq_relayout(m, lv["sites"].shape[0], dptr(lv["sites"]), dptr(lv["off_d"]),
-                                           lv["stride"], dptr(lv["chi"]), dptr(sites), dptr(fin["off_d"]),
-                                           fin["stride"], dptr(r32), stream_ptr()))
+            nl = lv["chi"].shape[0]
+            if lv.get("packed") is not None:
+                N.check(N.lib().mpskq_unpack_exact(m, nl, dptr(lv["packed"]), dptr(lv["state_off"]), dptr(lv["chi"]),
+                                                   dptr(sites), dptr(fin["off_d"]), fin["stride"], dptr(r32),
+                                                   stream_ptr()))
+            else:
+                N.check(N.lib().mpskq_relayout(m, nl, dptr(lv["sites"]), dptr(lv["off_d"]), lv["stride"],
+                                               dptr(lv["chi"]), dptr(sites), dptr(fin["off_d"]), fin["stride"],
+                                               dptr(r32), stream_ptr()))
             idx = lv["rows"] if lv["rows"] is not None else torch.arange(n, device=dev)
             chi.index_copy_(0, idx, lv["chi"])
             disc.index_copy_(0, idx, lv["disc"])
