@@ -44,7 +44,14 @@ namespace {
 using o1::kEnt;
 using o1::kLanes;
 using o1::kP;
-constexpr int kWarpsO1 = 8;            // bras per CTA tile
+#ifndef MPSKQ_O1_WARPS
+#define MPSKQ_O1_WARPS 8  // compute warps (= bras) per CTA tile: 8 (one CTA per SM) or 4 (two)
+#endif
+#ifndef MPSKQ_O1_STAGES
+#define MPSKQ_O1_STAGES 8  // ring depth in sites (power of two)
+#endif
+constexpr int kWarpsO1 = MPSKQ_O1_WARPS;        // bras per CTA tile
+constexpr int kCtasO1 = kWarpsO1 == 4 ? 2 : 1;  // resident CTAs per SM
 
 // --------------------------------------------------------------- packing
 // sim layout -> [site][block][entry][lane] (double2), zero padded to 4x2x4
@@ -254,7 +261,7 @@ __global__ void pack_bra_kernel(const double2* __restrict__ sites, const int32_t
   }
 }
 
-constexpr int kStages = 8;  // power of two: ring index = counter & 7
+constexpr int kStages = MPSKQ_O1_STAGES;  // power of two: ring index = counter & (kStages - 1)
 constexpr uint32_t kKetBytes = kEnt * kLanes * sizeof(double2);   // 16 KB per site
 constexpr uint32_t kBraBytes = kWarpsO1 * kEnt * sizeof(double2);  // 4 KB per site
 inline size_t o1_smem_bytes(int m) {
@@ -291,14 +298,9 @@ struct O1Args {
 // every compute warp could refill slots through a CAS on a shared counter,
 // ran 147.8 ms at N=6400 against 142 ms for this one, `profiles/r02_ab_o1_ws.txt`.)
 constexpr int kThreadsO1Ws = (kWarpsO1 + 4) * 32;
-#ifndef MPSKQ_O1_CN
-#define MPSKQ_O1_CN 0  // A/B knob: bra bonds + ket-block narrow flags in one shared table
-#endif
-#ifndef MPSKQ_O1_PSLEEP
-#define MPSKQ_O1_PSLEEP 0  // A/B knob: producer polls the empty barriers with this nanosleep (0: try_wait)
-#endif
 
-__global__ void __launch_bounds__(kThreadsO1Ws, 1) overlap_o1_kernel(O1Args a) {
+
+__global__ void __launch_bounds__(kThreadsO1Ws, kCtasO1) overlap_o1_kernel(O1Args a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* sket = reinterpret_cast<double2*>(smem_raw);
   double2* sbra = sket + kStages * kEnt * kLanes;
@@ -329,15 +331,7 @@ __global__ void __launch_bounds__(kThreadsO1Ws, 1) overlap_o1_kernel(O1Args a) {
         const double2* bb = a.bra + (int64_t)tl.x * kWarpsO1 * kEnt;
         for (int site = 0; site < m; ++site, ++q) {
           const uint32_t buf = q & (kStages - 1);
-          if (q >= kStages) {
-#if MPSKQ_O1_PSLEEP
-            // poll politely: the producer shares an SM sub-partition with two
-            // compute warps, and a freed slot has kStages - 1 sites of slack
-            while (!mbar_test(&empty[buf], ((q / kStages) - 1) & 1)) __nanosleep(MPSKQ_O1_PSLEEP);
-#else
-            mbar_wait(&empty[buf], ((q / kStages) - 1) & 1);
-#endif
-          }
+          if (q >= kStages) mbar_wait(&empty[buf], ((q / kStages) - 1) & 1);
           mbar_arrive_expect_tx(&full[buf], kKetBytes + kBraBytes);
           bulk_g2s(sket + buf * kEnt * kLanes, kb + site * kstride, kKetBytes, &full[buf]);
           bulk_g2s(sbra + buf * kWarpsO1 * kEnt, bb + site * bstride, kBraBytes, &full[buf]);
@@ -347,7 +341,10 @@ __global__ void __launch_bounds__(kThreadsO1Ws, 1) overlap_o1_kernel(O1Args a) {
     return;
   }
   // ---------------- compute warpgroups
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 240;\n" ::: "memory");
+  if constexpr (kCtasO1 == 1)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 240;\n" ::: "memory");
+  else
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
   uint32_t it = 0;  // sites this warp consumed (ring position + phase)
   int32_t* mychi = schi + warp * (m + 1);
   for (int64_t k = 0; k < my_tiles; ++k) {
@@ -357,14 +354,7 @@ __global__ void __launch_bounds__(kThreadsO1Ws, 1) overlap_o1_kernel(O1Args a) {
     const int64_t ic = i < a.n_bras ? i : a.n_bras - 1;
     const int64_t ib = a.bperm ? a.bperm[ic] : ic;  // bra index of this warp
     const uint8_t* narrow = a.kb_narrow + (int64_t)tile.y * (m + 1);
-#if MPSKQ_O1_CN
-    // bra bond in the low byte, the ket block's narrow flag in bit 8: one
-    // shared load per site instead of a shared and two global loads
-    for (int b = lane; b <= m; b += kLanes)
-      mychi[b] = __ldg(a.bra_chi + ib * (m + 1) + b) | ((int32_t)__ldg(narrow + b) << 8);
-#else
     for (int b = lane; b <= m; b += kLanes) mychi[b] = __ldg(a.bra_chi + ib * (m + 1) + b);
-#endif
     __syncwarp();
     double2 env[kP][kP];
 #pragma unroll
@@ -372,18 +362,9 @@ __global__ void __launch_bounds__(kThreadsO1Ws, 1) overlap_o1_kernel(O1Args a) {
 #pragma unroll
       for (int y = 0; y < kP; ++y) env[x][y] = make_double2(x == 0 && y == 0 ? 1.0 : 0.0, 0.0);
     int na = 1;  // chi_s of the bra (warp-uniform)
-#if MPSKQ_O1_CN
-    bool nar_l = (mychi[0] >> 8) != 0;
-#endif
     for (int s = 0; s < m; ++s) {
-#if MPSKQ_O1_CN
-      const int cn1 = mychi[s + 1];
-      const int na1 = cn1 & 0xff;
-      const bool nar_r = (cn1 >> 8) != 0;
-#else
       const int na1 = mychi[s + 1];
       const bool nar_l = __ldg(narrow + s) != 0, nar_r = __ldg(narrow + s + 1) != 0;
-#endif
       const uint32_t buf = it & (kStages - 1);
       mbar_wait(&full[buf], (it / kStages) & 1);
       const double2* B = sket + buf * kEnt * kLanes + lane;  // B[e] at B[e * 32]
@@ -401,9 +382,6 @@ __global__ void __launch_bounds__(kThreadsO1Ws, 1) overlap_o1_kernel(O1Args a) {
       if (lane == 0) mbar_arrive(&empty[buf]);
       ++it;
       na = na1;
-#if MPSKQ_O1_CN
-      nar_l = nar_r;
-#endif
     }
     const bool train = a.kind == MPSKQ_KIND_TRAIN;
     const bool valid = i < a.n_bras && j < a.n_kets && (!train || i < j);
@@ -796,7 +774,7 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
                  a.n_bras, a.n_kets, npb, nbk, m, a.kind,
                  a.out_mode, dtiles + band_tiles[b], nt, static_cast<double*>(ordered), a.n_kets,
                  bperm, kperm, static_cast<const uint8_t*>(narrow)};
-        overlap_o1_kernel<<<(int)std::min<int64_t>(nt, sms), kThreadsO1Ws, smem, sb>>>(o);
+        overlap_o1_kernel<<<(int)std::min<int64_t>(nt, (int64_t)sms * kCtasO1), kThreadsO1Ws, smem, sb>>>(o);
       }
       cudaEventRecord(evs[b], sb);
       cudaStreamWaitEvent(side, evs[b], 0);
@@ -850,7 +828,7 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // persistent: one CTA per SM walks the tile list (the ring stays warm)
-    const int grid = (int)std::min<int64_t>((int64_t)tiles.size(), sms);
+    const int grid = (int)std::min<int64_t>((int64_t)tiles.size(), (int64_t)sms * kCtasO1);
     overlap_o1_kernel<<<grid, kThreadsO1Ws, smem, st>>>(o);
     const int32_t* bpos = train ? static_cast<const int32_t*>(kinv) : nullptr;
     const int rows = (int)std::min<int64_t>(a.n_bras, 148 * 32);
