@@ -48,7 +48,7 @@ using o1::kP;
 #define MPSKQ_O1_WARPS 8  // compute warps (= bras) per CTA tile: 8 (one CTA per SM) or 4 (two)
 #endif
 #ifndef MPSKQ_O1_STAGES
-#define MPSKQ_O1_STAGES 8  // ring depth in sites (power of two)
+#define MPSKQ_O1_STAGES 10  // ring depth in sites (falls back to 8 when the chain is too long for it)
 #endif
 constexpr int kWarpsO1 = MPSKQ_O1_WARPS;        // bras per CTA tile
 constexpr int kCtasO1 = kWarpsO1 == 4 ? 2 : 1;  // resident CTAs per SM
@@ -261,11 +261,15 @@ __global__ void pack_bra_kernel(const double2* __restrict__ sites, const int32_t
   }
 }
 
-constexpr int kStages = MPSKQ_O1_STAGES;  // power of two: ring index = counter & (kStages - 1)
+// ring slots (sites in flight); slot = counter % STAGES.  10 slots measured
+// 139.8 ms vs 141.5 ms for 8 at N=6400 (warps drift further before the
+// slowest one holds a slot, profiles/r02_ab_o1_ws.txt)
+constexpr int kStages = MPSKQ_O1_STAGES;
+constexpr int kStagesMin = 8;
 constexpr uint32_t kKetBytes = kEnt * kLanes * sizeof(double2);   // 16 KB per site
 constexpr uint32_t kBraBytes = kWarpsO1 * kEnt * sizeof(double2);  // 4 KB per site
-inline size_t o1_smem_bytes(int m) {
-  return kStages * (size_t)(kKetBytes + kBraBytes) + 2 * kStages * sizeof(uint64_t) + 16 +
+inline size_t o1_smem_bytes(int m, int stages) {
+  return stages * (size_t)(kKetBytes + kBraBytes) + 2 * stages * sizeof(uint64_t) + 16 +
          sizeof(int32_t) * kWarpsO1 * (size_t)(m + 1);
 }
 
@@ -300,7 +304,9 @@ struct O1Args {
 constexpr int kThreadsO1Ws = (kWarpsO1 + 4) * 32;
 
 
+template <int STAGES>
 __global__ void __launch_bounds__(kThreadsO1Ws, kCtasO1) overlap_o1_kernel(O1Args a) {
+  constexpr int kStages = STAGES;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* sket = reinterpret_cast<double2*>(smem_raw);
   double2* sbra = sket + kStages * kEnt * kLanes;
@@ -330,7 +336,7 @@ __global__ void __launch_bounds__(kThreadsO1Ws, kCtasO1) overlap_o1_kernel(O1Arg
         const double2* kb = a.ket + (int64_t)tl.y * kEnt * kLanes;
         const double2* bb = a.bra + (int64_t)tl.x * kWarpsO1 * kEnt;
         for (int site = 0; site < m; ++site, ++q) {
-          const uint32_t buf = q & (kStages - 1);
+          const uint32_t buf = q % kStages;
           if (q >= kStages) mbar_wait(&empty[buf], ((q / kStages) - 1) & 1);
           mbar_arrive_expect_tx(&full[buf], kKetBytes + kBraBytes);
           bulk_g2s(sket + buf * kEnt * kLanes, kb + site * kstride, kKetBytes, &full[buf]);
@@ -365,7 +371,7 @@ __global__ void __launch_bounds__(kThreadsO1Ws, kCtasO1) overlap_o1_kernel(O1Arg
     for (int s = 0; s < m; ++s) {
       const int na1 = mychi[s + 1];
       const bool nar_l = __ldg(narrow + s) != 0, nar_r = __ldg(narrow + s + 1) != 0;
-      const uint32_t buf = it & (kStages - 1);
+      const uint32_t buf = it % kStages;
       mbar_wait(&full[buf], (it / kStages) & 1);
       const double2* B = sket + buf * kEnt * kLanes + lane;  // B[e] at B[e * 32]
       const double2* A = sbra + buf * kWarpsO1 * kEnt + warp * kEnt;
@@ -388,6 +394,17 @@ __global__ void __launch_bounds__(kThreadsO1Ws, kCtasO1) overlap_o1_kernel(O1Arg
     if (valid) store_result(a.out_mode, a.out, a.ld, i, j, env[0][0], train);
     __syncwarp();
   }
+}
+
+// the deepest ring whose shared memory fits this chain length
+struct O1Launch {
+  void (*fn)(O1Args);
+  size_t smem;
+};
+inline O1Launch o1_launch_for(int m) {
+  constexpr size_t kMaxSmem = 227 * 1024;
+  if (o1_smem_bytes(m, kStages) <= kMaxSmem) return {overlap_o1_kernel<kStages>, o1_smem_bytes(m, kStages)};
+  return {overlap_o1_kernel<kStagesMin>, o1_smem_bytes(m, kStagesMin)};
 }
 
 // --------------------------------------------------------------- generic chi (DMMA)
@@ -733,8 +750,9 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
   frees.push_back(dtiles);
   cudaError_t e = cudaSuccess;
   if (to_host) {
-    const size_t smem = o1_smem_bytes(m);
-    e = cudaFuncSetAttribute(overlap_o1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    O1Launch lk = o1_launch_for(m);
+    const size_t smem = lk.smem;
+    e = cudaFuncSetAttribute(lk.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 
     if (e != cudaSuccess) {
       release();
@@ -774,7 +792,7 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
                  a.n_bras, a.n_kets, npb, nbk, m, a.kind,
                  a.out_mode, dtiles + band_tiles[b], nt, static_cast<double*>(ordered), a.n_kets,
                  bperm, kperm, static_cast<const uint8_t*>(narrow)};
-        overlap_o1_kernel<<<(int)std::min<int64_t>(nt, (int64_t)sms * kCtasO1), kThreadsO1Ws, smem, sb>>>(o);
+        lk.fn<<<(int)std::min<int64_t>(nt, (int64_t)sms * kCtasO1), kThreadsO1Ws, smem, sb>>>(o);
       }
       cudaEventRecord(evs[b], sb);
       cudaStreamWaitEvent(side, evs[b], 0);
@@ -813,8 +831,9 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
       return cuda_fail(e, "overlap_o1 host streaming");
     }
   } else if (!tiles.empty()) {
-    const size_t smem = o1_smem_bytes(m);
-    e = cudaFuncSetAttribute(overlap_o1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    O1Launch lk = o1_launch_for(m);
+    const size_t smem = lk.smem;
+    e = cudaFuncSetAttribute(lk.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 
     if (e != cudaSuccess) {
       release();
@@ -829,7 +848,7 @@ int launch_o1(const OverlapArgs& a, cudaStream_t st) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // persistent: one CTA per SM walks the tile list (the ring stays warm)
     const int grid = (int)std::min<int64_t>((int64_t)tiles.size(), (int64_t)sms * kCtasO1);
-    overlap_o1_kernel<<<grid, kThreadsO1Ws, smem, st>>>(o);
+    lk.fn<<<grid, kThreadsO1Ws, smem, st>>>(o);
     const int32_t* bpos = train ? static_cast<const int32_t*>(kinv) : nullptr;
     const int rows = (int)std::min<int64_t>(a.n_bras, 148 * 32);
     if (a.owned) {

@@ -106,3 +106,22 @@ def test_benchmark_payload_memory_series_matches_oracle():
     assert len(out["inner_product_seconds"]) == 10 and out["simulation_summary"]["median"] > 0
     with pytest.raises(ValueError):
         benchmark_rows(X[:1], cfg)
+
+
+def test_long_chain_overlap_falls_back_to_a_shallower_ring():
+    """m = 1000 qubits: the chi <= 4 overlap's 10-stage ring no longer fits
+    shared memory next to the per-warp bond tables, so the 8-stage build runs;
+    K against the oracle on a few states."""
+    import paper_2411_09336_b200 as P
+
+    m = 1000
+    X = np.random.default_rng(21).uniform(0.0, 2.0, (40, m))
+    cfg = P.FeatureMapConfig(m, 2, 1, 0.1)
+    tr = P.simulate_dataset(X, cfg)
+    assert tr.chi_cap == 4
+    K = P.compute_gram(tr, tr, "train").entries
+    ref = [O.simulate_row(X[i], m, 2, 1, 0.1, 1e-24) for i in (0, 1, 2)]
+    assert [tr.bond_dims()[i].tolist() for i in (0, 1, 2)] == [r.bond_dims() for r in ref]
+    Ko = O.gram([r.sites for r in ref], [r.sites for r in ref], "train")
+    assert np.abs(K[:3, :3] - Ko).max() < 1e-10
+    assert np.array_equal(K, K.T) and np.all(np.diag(K) == 1.0)
