@@ -419,15 +419,24 @@ def simulate_program(prog: Program, coef, budget: float, chi_max: int = 0,
             phase=torch.zeros((nl, 3), dtype=torch.int64, device=dev),
             flops=torch.zeros(nl, dtype=torch.float64, device=dev),
         )
-        with Timer() as tm:
-            N.check(
-                N.lib().mpskq_run_program(
-                    m, cap, dptr(ops_d), prog.ops.shape[0], prog.n_gates, dptr(coef_l), prog.n_params, nl,
-                    float(budget), int(chi_max), dptr(off_d), stride, 0, dptr(lv["sites"]), dptr(lv["chi"]),
-                    dptr(lv["disc"]), dptr(lv["peak"]), dptr(lv["status"]), dptr(lv["elog"]),
-                    dptr(lv["phase"]), dptr(lv["flops"]), stream_ptr(),
-                )
+        def run():
+            return N.lib().mpskq_run_program(
+                m, cap, dptr(ops_d), prog.ops.shape[0], prog.n_gates, dptr(coef_l), prog.n_params, nl,
+                float(budget), int(chi_max), dptr(off_d), stride, 0, dptr(lv["sites"]), dptr(lv["chi"]),
+                dptr(lv["disc"]), dptr(lv["peak"]), dptr(lv["status"]), dptr(lv["elog"]),
+                dptr(lv["phase"]), dptr(lv["flops"]), stream_ptr(),
             )
+
+        with Timer() as tm:
+            st_code = run()
+            if st_code == N.ERR_CUDA and b"out of memory" in (N.lib().mpskq_last_error() or b""):
+                # the simulator's per-CTA workspaces come from the stream-ordered
+                # pool; blocks torch's caching allocator keeps for reuse are not
+                # visible to it: hand them back and retry once
+                torch.cuda.synchronize()
+                torch.cuda.empty_cache()
+                st_code = run()
+            N.check(st_code)
         seconds += tm.seconds()
         over = _check_states(lv["status"].cpu().numpy())
         levels.append(lv)

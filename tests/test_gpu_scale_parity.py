@@ -5,13 +5,14 @@
    (peak chi 85+, capacity 96/128) and 1e-16 (capacity 32/48), config 5 at
    d = 1, 2, 3, 5 and a second seed at d = 6, 7, 8.  Bond dims identical per
    site, accumulated discard and K within tolerance.
-2. Full-size scans: every row of the headline (6400), config 2 (800 + 200),
+2. Full-size scans: every row of the headline (6400 + 1600), config 2 (800 + 200),
    config 3 (1600 + 400) and 64 rows per interaction distance of config 5
    (d = 5..8) simulated on the GPU and by the oracle (bitwise the reference,
    tests/test_oracle.py) in a host process pool; the number of states whose
    bond dimensions differ ("truncation flips") is recorded in
    gpurun_out/scale_parity_<name>.json and must be zero; K is compared on
-   every pair of a 24-state sample.
+   every pair of a 24-state sample (and, with test rows, the test kernel on 8
+   test rows against it).
 
 Tolerances (BASELINE.json north_star): 1e-10 for budgets 0 / 1e-24, 1e-6 at
 the 1e-16 fidelity cutoff.
@@ -91,7 +92,7 @@ def test_large_chi_fixture_matches_reference(name):
 
 SCANS = {
     # name: (m, d, gamma, budget, N_train, N_test)
-    "headline_m165_d1": (165, 1, 0.1, 1e-24, 6400, 0),
+    "headline_m165_d1": (165, 1, 0.1, 1e-24, 6400, 1600),
     "config2_m50_d2": (50, 2, 0.1, 1e-24, 800, 200),
     "config3_m100_d4": (100, 4, 0.1, 1e-16, 1600, 400),
     "config5_m100_d5": (100, 5, 0.1, 1e-16, 64, 0),
@@ -126,11 +127,17 @@ def test_every_state_matches_oracle_bond_dims(name):
         chi = np.vstack([chi, te.bond_dims()])
         disc = np.concatenate([disc, te.discard.cpu().numpy()])
     K = P.compute_gram(tr, tr, "train").entries
+    Kt = P.compute_gram(te, tr, "test").entries if mt else None
     t_gpu = time.time() - t0
 
     flips = [int(i) for i in np.nonzero(np.any(chi != ref_chi, axis=1))[0]]
     Ko = O.gram([ref_sites[i] for i in sample], [ref_sites[i] for i in sample], "train")
     k_err = float(np.abs(K[np.ix_(sample, sample)] - Ko).max())
+    if mt:  # test kind: a sample of test rows against the sampled train rows
+        tsample = np.sort(rng.choice(mt, min(mt, 8), replace=False))
+        _, _, tsites = oracle_states(Xt[tsample], m, 2, d, gamma, budget, keep=range(len(tsample)))
+        Kto = O.gram([tsites[k] for k in range(len(tsample))], [ref_sites[i] for i in sample], "test")
+        k_err = max(k_err, float(np.abs(Kt[np.ix_(tsample, sample)] - Kto).max()))
     rec = {
         "config": name, "m": m, "d": d, "gamma": gamma, "budget": budget, "states": int(rows.shape[0]),
         "bond_dim_flips": len(flips), "flipped_rows": flips[:32],

@@ -53,6 +53,7 @@ def main(names):
     peak = fp64_peak_tflops(N.lib(), torch)
     res = {"fp64_peak_tflops_measured": peak}
     for name in names:
+        torch.cuda.empty_cache()  # each config starts from the same free HBM
         m, d, gamma, budget, n = CONFIGS[name]
         cfg = P.FeatureMapConfig(m, 2, d, gamma)
         X = np.random.default_rng(0).uniform(0.0, 2.0, (n, m))
