@@ -266,9 +266,6 @@ __global__ void pack_bra_kernel(const double2* __restrict__ sites, const int32_t
 // slowest one holds a slot, profiles/r02_ab_o1_ws.txt)
 constexpr int kStages = MPSKQ_O1_STAGES;
 constexpr int kStagesMin = 8;
-#ifndef MPSKQ_O1_WAIT_NS
-#define MPSKQ_O1_WAIT_NS 0  // A/B knob: suspend-time hint of the ring waits (0: plain try_wait)
-#endif
 constexpr uint32_t kKetBytes = kEnt * kLanes * sizeof(double2);   // 16 KB per site
 constexpr uint32_t kBraBytes = kWarpsO1 * kEnt * sizeof(double2);  // 4 KB per site
 inline size_t o1_smem_bytes(int m, int stages) {
@@ -340,11 +337,7 @@ __global__ void __launch_bounds__(kThreadsO1Ws, kCtasO1) overlap_o1_kernel(O1Arg
         const double2* bb = a.bra + (int64_t)tl.x * kWarpsO1 * kEnt;
         for (int site = 0; site < m; ++site, ++q) {
           const uint32_t buf = q % kStages;
-#if MPSKQ_O1_WAIT_NS
-          if (q >= kStages) mbar_wait_hint(&empty[buf], ((q / kStages) - 1) & 1, MPSKQ_O1_WAIT_NS);
-#else
           if (q >= kStages) mbar_wait(&empty[buf], ((q / kStages) - 1) & 1);
-#endif
           mbar_arrive_expect_tx(&full[buf], kKetBytes + kBraBytes);
           bulk_g2s(sket + buf * kEnt * kLanes, kb + site * kstride, kKetBytes, &full[buf]);
           bulk_g2s(sbra + buf * kWarpsO1 * kEnt, bb + site * bstride, kBraBytes, &full[buf]);
@@ -379,11 +372,7 @@ __global__ void __launch_bounds__(kThreadsO1Ws, kCtasO1) overlap_o1_kernel(O1Arg
       const int na1 = mychi[s + 1];
       const bool nar_l = __ldg(narrow + s) != 0, nar_r = __ldg(narrow + s + 1) != 0;
       const uint32_t buf = it % kStages;
-#if MPSKQ_O1_WAIT_NS
-      mbar_wait_hint(&full[buf], (it / kStages) & 1, MPSKQ_O1_WAIT_NS);
-#else
       mbar_wait(&full[buf], (it / kStages) & 1);
-#endif
       const double2* B = sket + buf * kEnt * kLanes + lane;  // B[e] at B[e * 32]
       const double2* A = sbra + buf * kWarpsO1 * kEnt + warp * kEnt;
       double2 T[kP][2][kP];
