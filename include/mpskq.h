@@ -101,8 +101,9 @@ int mpskq_half_angle_coefficients(const double* angles, int64_t n, double* coef)
 
 /* Device twin of the two calls above: X_dev (n_rows x m, device) ->
  * coef_dev (n_rows x n_params x {cos, sin}), angles bitwise as above, sin/cos
- * by CUDA (<= 2 ulp from libm).  *bad_dev (device int, caller zeroes it) is
- * set non-zero if a feature lies outside [0, 2] or is not finite.          */
+ * by CUDA (<= 2 ulp from libm).  *bad_dev (device int, caller zeroes it)
+ * gets bit 1 if a finite feature lies outside [0, 2] and bit 2 if a feature
+ * is not finite (build_circuit's checks, ansatz.py:118-124).              */
 int mpskq_feature_map_coefficients_device(const double* X_dev, int64_t n_rows, int m, int r,
                                           int d, double gamma, double* coef_dev, int* bad_dev,
                                           void* stream);

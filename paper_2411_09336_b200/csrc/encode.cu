@@ -25,7 +25,10 @@ __global__ void encode_kernel(const double* __restrict__ X, int64_t n_rows, int 
     double angle;
     if (p < m) {
       const double xq = x[p];
-      if (!(xq >= 0.0 && xq <= 2.0)) atomicOr(bad, 1);  // also catches NaN
+      if (!isfinite(xq))
+        atomicOr(bad, 2);  // build_circuit's finite check (ansatz.py:121-122)
+      else if (xq < 0.0 || xq > 2.0)
+        atomicOr(bad, 1);  // ... and its [0, 2] range check (:123-124)
       angle = __dmul_rn(rz_scale, xq);
     } else {
       const int2 e = edges[p - m];

@@ -529,14 +529,6 @@ int program_for(int m, int r, int d, std::vector<int32_t>& ops, int64_t& n_gates
     if (s_ != MPSKQ_OK) return s_; \
   } while (0)
 
-int check_rows_host(const double* X, int64_t n, int m) {
-  for (int64_t i = 0; i < n * m; ++i) {
-    if (!std::isfinite(X[i])) return fail(MPSKQ_ERR_INVALID, "features must be finite");
-    if (X[i] < 0.0 || X[i] > 2.0)
-      return fail(MPSKQ_ERR_INVALID, "features must lie in [0, 2]; rescale the data first");
-  }
-  return MPSKQ_OK;
-}
 
 // K of the given device states into host memory K_out (n_bras x n_kets).
 // Pinned (page-locked, device-mapped) K_out on the chi <= 4 path: the
@@ -598,8 +590,8 @@ extern "C" int mpskq_gram_host(int kind, int m, int r, int d, double gamma, doub
     n_kets = n_bras;
   }
   if (n_bras < 0 || n_kets < 0) return fail(MPSKQ_ERR_INVALID, "negative row count");
-  ST(check_rows_host(X_bras, n_bras, m));
-  if (!train) ST(check_rows_host(X_kets, n_kets, m));
+  // the rows are validated on the device by the encoder (bad flag, read with
+  // the first simulation status): a host scan of N x m doubles cost ~1 ms
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t n_all = train ? n_bras : n_bras + n_kets;
   {
@@ -694,8 +686,12 @@ extern "C" int mpskq_gram_host(int kind, int m, int r, int d, double gamma, doub
                       L->doff.as<int64_t>(), L->stride, L->sites.as<double>(), L->chi.as<int32_t>(),
                       L->disc.as<double>(), L->peak.as<int32_t>(), L->status.as<int32_t>(), nullptr, stream));
     std::vector<int32_t> hstatus(L->n);
+    int hbad = 0;
     CK(cudaMemcpyAsync(hstatus.data(), L->status.p, sizeof(int32_t) * L->n, cudaMemcpyDeviceToHost, st));
+    if (levels.empty()) CK(cudaMemcpyAsync(&hbad, dbad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (hbad & 2) return fail(MPSKQ_ERR_INVALID, "features must be finite");
+    if (hbad & 1) return fail(MPSKQ_ERR_INVALID, "features must lie in [0, 2]; rescale the data first");
     std::vector<int32_t> next;
     for (int64_t i = 0; i < L->n; ++i) {
       if (hstatus[i] == MPSKQ_STATE_NONFINITE) return fail(MPSKQ_ERR_NUMERIC, "tensor has non-finite entries");

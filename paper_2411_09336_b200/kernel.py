@@ -359,9 +359,9 @@ def run_distributed(X_bras, X_kets, cfg: FeatureMapConfig, schedule: TileSchedul
                                 and X_bras.strides == X_kets.strides)
     if schedule.kind == "train" and not same and not np.array_equal(X_bras, X_kets):
         raise ValueError("train kind requires identical bra and ket rows")
-    for X in ((X_bras,) if same else (X_bras, X_kets)):
-        if not np.all(np.isfinite(X)):
-            raise ValueError("features must be finite")
+    # finiteness and the [0, 2] range are checked where the rows are encoded
+    # (the device encoder on one GPU, simulate_rows on several), with the
+    # reference's messages (kernel.py:138-144, ansatz.py:121-124)
     from . import distributed
 
     try:

@@ -148,3 +148,32 @@ def test_benchmark_reports_real_per_sample_times():
         benchmark_rows(np.full((2, 12), np.nan), cfg)
     with pytest.raises(ValueError, match=r"\[0, 2\]"):
         benchmark_rows(np.full((2, 12), 3.0), cfg)
+
+
+def test_run_distributed_row_errors_through_the_native_path():
+    """Non-finite / out-of-range rows are caught by the device encoder of the
+    one-GPU native call with the reference's messages (kernel.py:138-144,
+    ansatz.py:121-124); non-finite wins when both occur."""
+    import paper_2411_09336_b200 as P
+
+    cfg = P.FeatureMapConfig(6, 1, 2, 0.5)
+    X = np.random.default_rng(3).uniform(0.0, 2.0, (5, 6))
+    sched = P.make_schedule(5, 5, 1, "round_robin", "train")
+    bad = X.copy()
+    bad[2, 3] = np.nan
+    with pytest.raises(ValueError, match="finite"):
+        P.run_distributed(bad, bad, cfg, sched)
+    bad = X.copy()
+    bad[4, 0] = 3.0
+    with pytest.raises(ValueError, match=r"\[0, 2\]"):
+        P.run_distributed(bad, bad, cfg, sched)
+    bad[1, 1] = np.inf
+    with pytest.raises(ValueError, match="finite"):
+        P.run_distributed(bad, bad, cfg, sched)
+    Xt = np.random.default_rng(4).uniform(0.0, 2.0, (2, 6))
+    Xt[0, 0] = -0.5
+    with pytest.raises(ValueError, match=r"\[0, 2\]"):
+        P.run_distributed(Xt, X, cfg, P.make_schedule(2, 5, 1, "round_robin", "test"))
+    # a good call after the failures still works (no sticky state)
+    K = P.run_distributed(X, X, cfg, sched).entries
+    assert np.all(np.diag(K) == 1.0)
