@@ -125,14 +125,19 @@ struct GlobalWs {
       (direct_w ? 2 : 1) * (int64_t)(2 * CAP) * (2 * CAP) + 2 * (int64_t)CAP * CAP;
 };
 
-// Capacities 48 and 80-128 keep only theta/C on the fast side: the Jacobi
+// Capacities 24-48 and 80-128 keep only theta/C on the fast side: the Jacobi
 // rotations are logged to a per-CTA global buffer and replayed on the identity
 // after the C-side factor has been written out (W then reuses C's space).
-// (Using it from capacity 12 up doubles the resident states but the replay
-// costs about as much as it saves: measured neutral to negative.)
+// Capacities 24 and 32 use it too: halving the shared carve-out doubles the
+// resident states (d=5 cap 32: 3.38 -> 2.56 s; d=4 cap 24: 1.54 -> 1.43 s).
+// The log is per CTA, so it needs one state per CTA (NT > 32): the
+// lockstepped multi-state CTAs of capacities <= 16 would share it.
+#ifndef MPSKQ_LOGW_ABOVE
+#define MPSKQ_LOGW_ABOVE 16  // capacities above this log the Jacobi rotations (A/B knob)
+#endif
 template <int CAP>
 struct LogW {
-  static constexpr bool value = CAP > 32 && !GlobalWs<CAP>::direct_w;
+  static constexpr bool value = CAP > MPSKQ_LOGW_ABOVE && !GlobalWs<CAP>::direct_w && NtFor<CAP>::value > 32;
   static constexpr int64_t entries = (int64_t)kMaxSweeps * (2 * CAP) * CAP;  // sweeps x rounds x pairs
 };
 
@@ -155,7 +160,7 @@ struct Smem {
   int* piv;      // LD: inverse column order of the pivoted QR
   int* ibuf;     // 4: keep
   int* chi;      // m + 1
-  double4* rlog;  // per-CTA rotation log (capacities > 32 only)
+  double4* rlog;  // per-CTA rotation log (LogW capacities only)
 
   __host__ __device__ static size_t bytes(int m) {
     size_t b = GlobalWs<CAP>::value
