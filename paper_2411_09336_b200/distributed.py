@@ -254,8 +254,11 @@ def ring_plan(world: int, rank: int, kind: str) -> list:
     return plan
 
 
-def _ring_shift(tensors: list, rank: int, world: int, group=None) -> list:
-    """Send every tensor to rank+1 and receive same-shaped ones from rank-1."""
+def _ring_shift_start(tensors: list, rank: int, world: int, group=None) -> tuple:
+    """Post the sends of every tensor to rank+1 and the receives of same-shaped
+    ones from rank-1; returns the pending (works, received, device) for
+    _ring_shift_finish.  On NCCL the transfer runs on the communicator's
+    stream, so kernels launched before the finish overlap it."""
     import torch.distributed as dist
 
     host = _host_collectives(group)
@@ -265,14 +268,24 @@ def _ring_shift(tensors: list, rank: int, world: int, group=None) -> list:
     for a, b in zip(src, dst):
         ops.append(dist.P2POp(dist.isend, a, (rank + 1) % world, group))
         ops.append(dist.P2POp(dist.irecv, b, (rank - 1) % world, group))
-    for w in dist.batch_isend_irecv(ops):
+    return dist.batch_isend_irecv(ops), dst, tensors[0].device
+
+
+def _ring_shift_finish(pending: tuple) -> list:
+    works, dst, dev = pending
+    for w in works:
         w.wait()
-    dev = tensors[0].device
     return [b.to(dev) for b in dst]
 
 
+def _ring_shift(tensors: list, rank: int, world: int, group=None) -> list:
+    """Send every tensor to rank+1 and receive same-shaped ones from rank-1."""
+    return _ring_shift_finish(_ring_shift_start(tensors, rank, world, group))
+
+
 def _ring_gram(full_kets, bras, nb_lo, kets_counts, cfg, kind, rank, world, group, K_dev):
-    """Fill this rank's ring blocks of K_dev; returns seconds spent exchanging."""
+    """Fill this rank's ring blocks of K_dev; returns host seconds spent posting
+    and waiting on the shifts (the transfer itself overlaps the block)."""
     from .mps import MpsBatch, overlap_matrix
 
     mx = max(kets_counts)
@@ -286,6 +299,14 @@ def _ring_gram(full_kets, bras, nb_lo, kets_counts, cfg, kind, rank, world, grou
     # up to world // 2, test all of them
     plan = ring_plan(world, rank, kind)[: (world // 2 + 1 if kind == "train" else world)]
     for t, held, block in plan:
+        # post the shift of the held shard before computing on it, so the
+        # next shard travels while this block's overlaps run (reference
+        # analogue: round-robin step 0 computing the local block, kernel.py:225-227)
+        pending = None
+        if t < len(plan) - 1:
+            t0 = time.perf_counter()
+            pending = _ring_shift_start([pad_sites, pad_chi], rank, world, group)
+            comm += time.perf_counter() - t0
         c = kets_counts[held]
         if block is not None and c > 0 and len(bras) > 0:
             kets = MpsBatch(cfg.m, full_kets.chi_cap, full_kets.site_off, full_kets.stride, pad_sites[:c],
@@ -304,9 +325,9 @@ def _ring_gram(full_kets, bras, nb_lo, kets_counts, cfg, kind, rank, world, grou
                 K_dev[nb_lo : nb_lo + len(bras), k0:k1] = blk
                 if kind == "train":
                     K_dev[k0:k1, nb_lo : nb_lo + len(bras)] = blk.T
-        if t < len(plan) - 1:
+        if pending is not None:
             t0 = time.perf_counter()
-            pad_sites, pad_chi = _ring_shift([pad_sites, pad_chi], rank, world, group)
+            pad_sites, pad_chi = _ring_shift_finish(pending)
             comm += time.perf_counter() - t0
     return comm
 
