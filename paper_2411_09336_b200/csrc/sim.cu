@@ -49,10 +49,10 @@ constexpr int kNoConvergence = 1 << 30;  // flag bit in jacobi()'s round count
 #define MPSKQ_NT8 32
 #endif
 #ifndef MPSKQ_NT16
-#define MPSKQ_NT16 32
+#define MPSKQ_NT16 64
 #endif
 #ifndef MPSKQ_NT32
-#define MPSKQ_NT32 128
+#define MPSKQ_NT32 64
 #endif
 #ifndef MPSKQ_NT48
 #define MPSKQ_NT48 192
@@ -105,33 +105,43 @@ template <int CAP>
 struct NtFor {
   static constexpr int value =
       CAP <= 4 ? MPSKQ_NT4 : CAP <= 8 ? MPSKQ_NT8 : CAP <= 16 ? MPSKQ_NT16 : CAP <= 32 ? MPSKQ_NT32 : CAP <= 48 ? MPSKQ_NT48 : MPSKQ_NT128;
+  // the Jacobi pairs every column (G lanes per pair, G * n/2 <= NT) and
+  // several passes take one lane per column
+  static_assert(value >= 2 * CAP, "a state needs at least 2 * CAP threads");
 };
 
-// Capacities above 48: theta/C and the staging buffer no longer fit shared
-// memory; they live in a per-CTA global scratch (L2 resident), the small
-// per-op arrays stay in shared memory.
-// At capacity 64 W gets its own plane there too and is accumulated during
-// the Jacobi (no rotation log, no replay): d=7 sim 6.34 -> 5.48 s.  At 96 and
-// 128 the same change measured neutral / +2% (the per-round W rotation over
-// 2*CAP rows costs what the replay saved), so they keep the log.
+// Capacities above 12: theta/C, the staging buffer and W live in a per-CTA
+// global scratch (L2 resident), only the small per-op arrays in shared
+// memory, so residency is set by registers, not by the 2CAP x 2CAP planes:
+// d=6 (cap 48) 5.14 -> 3.25 s, plus 3 CTAs per SM at 192 threads -> 2.19 s;
+// d=5 (cap 32) 2.56 -> 1.63 s; d=4 (cap 24) 1.43 -> 1.17 s; with 64 threads
+// per state at capacities 12-32 (d=5 1.31 s, d=4 0.81 s, d=3 0.35 -> 0.27 s)
+// (`profiles/r02_ab_sim_global_ws.txt`).  Up to capacity 64 W gets its own
+// plane there and is accumulated during the Jacobi (no rotation log, no
+// replay): d=7 sim 6.34 -> 5.48 s.  At 96 and 128 the same change measured
+// neutral / +2% (the per-round W rotation over 2*CAP rows costs what the
+// replay saved), so they keep the log.
 #ifndef MPSKQ_DIRECT_W_MAX
 #define MPSKQ_DIRECT_W_MAX 64  // A/B knob
 #endif
+#ifndef MPSKQ_GLOBAL_WS_ABOVE
+#define MPSKQ_GLOBAL_WS_ABOVE 12  // A/B knob
+#endif
 template <int CAP>
 struct GlobalWs {
-  static constexpr bool value = CAP > 48;
+  // per-CTA slices: needs one state per CTA (NT > 32)
+  static constexpr bool value = CAP > MPSKQ_GLOBAL_WS_ABOVE && NtFor<CAP>::value > 32;
   static constexpr bool direct_w = value && CAP <= MPSKQ_DIRECT_W_MAX;
   static constexpr int64_t complexes =
       (direct_w ? 2 : 1) * (int64_t)(2 * CAP) * (2 * CAP) + 2 * (int64_t)CAP * CAP;
 };
 
-// Capacities 24-48 and 80-128 keep only theta/C on the fast side: the Jacobi
+// Capacities 80-128 keep only theta/C and the staging buffer: the Jacobi
 // rotations are logged to a per-CTA global buffer and replayed on the identity
 // after the C-side factor has been written out (W then reuses C's space).
-// Capacities 24 and 32 use it too: halving the shared carve-out doubles the
-// resident states (d=5 cap 32: 3.38 -> 2.56 s; d=4 cap 24: 1.54 -> 1.43 s).
-// The log is per CTA, so it needs one state per CTA (NT > 32): the
-// lockstepped multi-state CTAs of capacities <= 16 would share it.
+// (With W in shared memory, capacities 24 and 32 gained from the log too:
+// d=5 3.38 -> 2.56 s; the global workspace above superseded that.)  The log
+// is per CTA, so it needs one state per CTA (NT > 32).
 #ifndef MPSKQ_LOGW_ABOVE
 #define MPSKQ_LOGW_ABOVE 16  // capacities above this log the Jacobi rotations (A/B knob)
 #endif
@@ -1164,9 +1174,15 @@ struct SpcFor {
 // resident states per SM need <= 64 registers per thread.  Without the bound
 // ptxas takes 128 and halves the states in flight (measured +29% simulation
 // time at m=100 d=7 / d=8, tools/ab_sim_abi.py).
+#ifndef MPSKQ_MIN_CTAS_128
+#define MPSKQ_MIN_CTAS_128 1  // A/B knob: launch-bound CTAs per SM at 128 threads
+#endif
+#ifndef MPSKQ_MIN_CTAS_192
+#define MPSKQ_MIN_CTAS_192 3  // A/B knob: launch-bound CTAs per SM at 192 threads
+#endif
 template <int NT>
 struct MinCtasFor {
-  static constexpr int value = NT >= 512 ? 2 : 1;
+  static constexpr int value = NT >= 512 ? 2 : NT == 192 ? MPSKQ_MIN_CTAS_192 : NT == 128 ? MPSKQ_MIN_CTAS_128 : 1;
 };
 
 // GEN: programs of the state-level API (continue a given state, arbitrary

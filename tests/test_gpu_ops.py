@@ -106,7 +106,9 @@ def test_per_state_capacity_escalation():
 
     direct = simulate_rows(g["X"], cfg, 1e-24, chi_cap=12)
     Kd = P.compute_gram(direct, direct, "train").entries
-    assert np.abs(K - Kd).max() < 1e-14
+    # capacities 8 and 12 run different lanes per state (32 lockstepped vs
+    # 64), so the Jacobi's reduction order differs in the last bits
+    assert np.abs(K - Kd).max() < 1e-12
     assert np.array_equal(direct.bond_dims(), b.bond_dims())
 
 
