@@ -41,7 +41,10 @@ constexpr int kNoConvergence = 1 << 30;  // flag bit in jacobi()'s round count
 // the old 16/64/128/256/384 sped up capacity 4 (15.6 -> 13.7 ms at the
 // headline), 8 (34 -> 30 ms), 12-16 (28 -> 23 ms), 24-32 (1.84 -> 1.57 s) and
 // 48 (-3%); halving again was slower except at 12-16, and 4 lanes breaks the
-// capacity-4 Jacobi.  Capacities >= 64 keep 512.
+// capacity-4 Jacobi.  Round 2, with the workspace in global scratch (below):
+// 64 lanes at 12-32, 256 at 64-96 (3 states per SM); capacity 128 keeps 512
+// (its batches are small — 148 states at the 165-qubit d=6 budget-1e-24
+// case — so per-state latency rules: 256 lanes took 30 -> 48 s there).
 #ifndef MPSKQ_NT4
 #define MPSKQ_NT4 8
 #endif
@@ -56,6 +59,9 @@ constexpr int kNoConvergence = 1 << 30;  // flag bit in jacobi()'s round count
 #endif
 #ifndef MPSKQ_NT48
 #define MPSKQ_NT48 192
+#endif
+#ifndef MPSKQ_NT96
+#define MPSKQ_NT96 256  // capacities 64-96: 3 states per SM (d=7 9.8 -> 6.0 s at N=400)
 #endif
 #ifndef MPSKQ_NT128
 #define MPSKQ_NT128 512
@@ -104,7 +110,7 @@ __device__ __forceinline__ int ltid() {
 template <int CAP>
 struct NtFor {
   static constexpr int value =
-      CAP <= 4 ? MPSKQ_NT4 : CAP <= 8 ? MPSKQ_NT8 : CAP <= 16 ? MPSKQ_NT16 : CAP <= 32 ? MPSKQ_NT32 : CAP <= 48 ? MPSKQ_NT48 : MPSKQ_NT128;
+      CAP <= 4 ? MPSKQ_NT4 : CAP <= 8 ? MPSKQ_NT8 : CAP <= 16 ? MPSKQ_NT16 : CAP <= 32 ? MPSKQ_NT32 : CAP <= 48 ? MPSKQ_NT48 : CAP <= 96 ? MPSKQ_NT96 : MPSKQ_NT128;
   // the Jacobi pairs every column (G lanes per pair, G * n/2 <= NT) and
   // several passes take one lane per column
   static_assert(value >= 2 * CAP, "a state needs at least 2 * CAP threads");
@@ -1170,19 +1176,23 @@ struct SpcFor {
   static constexpr int value = NT <= 32 ? MPSKQ_SPC_THREADS / NT : 1;
 };
 
-// Capacities 64-128 (512 threads per state, theta in the L2 workspace): two
-// resident states per SM need <= 64 registers per thread.  Without the bound
+// Capacity 128 (512 threads per state, theta in the L2 workspace): two
+// resident states per SM need <= 64 registers per thread; capacities 64-96
+// (256 threads) bound three.  Without the bound
 // ptxas takes 128 and halves the states in flight (measured +29% simulation
 // time at m=100 d=7 / d=8, tools/ab_sim_abi.py).
 #ifndef MPSKQ_MIN_CTAS_128
 #define MPSKQ_MIN_CTAS_128 1  // A/B knob: launch-bound CTAs per SM at 128 threads
+#endif
+#ifndef MPSKQ_MIN_CTAS_256
+#define MPSKQ_MIN_CTAS_256 3  // A/B knob: launch-bound CTAs per SM at 256 threads
 #endif
 #ifndef MPSKQ_MIN_CTAS_192
 #define MPSKQ_MIN_CTAS_192 3  // A/B knob: launch-bound CTAs per SM at 192 threads
 #endif
 template <int NT>
 struct MinCtasFor {
-  static constexpr int value = NT >= 512 ? 2 : NT == 192 ? MPSKQ_MIN_CTAS_192 : NT == 128 ? MPSKQ_MIN_CTAS_128 : 1;
+  static constexpr int value = NT >= 512 ? 2 : NT == 256 ? MPSKQ_MIN_CTAS_256 : NT == 192 ? MPSKQ_MIN_CTAS_192 : NT == 128 ? MPSKQ_MIN_CTAS_128 : 1;
 };
 
 // GEN: programs of the state-level API (continue a given state, arbitrary
